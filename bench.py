@@ -1,0 +1,453 @@
+#!/usr/bin/env python3
+"""bench.py -- LUT-correction Gpixel/s (+ matmul TFLOP/s) on B200, next to the
+host-CPU reference path.
+
+Primary line (BASELINE.json metric): LUT image correction (LUT_GEN equalize +
+LUT_APPLY, i.e. LUT_CORRECT) of the config-C3 scene, 32768 x 32768 u16
+(ramp12 synthetic), row-band sharded over N GPUs: each rank histograms its
+band, the 65536-bin histograms are all-reduced over NCCL (the one exchange
+step the equalize LUT needs), every rank builds the identical LUT and
+applies it to its band.  One step = one full LUT_CORRECT of the scene.
+The matmul figure (config C2, FP32 4096^3 through the SIMT kernel, and the
+tensor-core path once built) rides along in the "matmul" object.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Timing: CUDA events on the stream the kernels are launched on, barrier +
+synchronize on both sides of the K timed steps, max over ranks.  Inputs are
+device-resident and larger than L2 (2 GiB / N per rank) -- no flush needed.
+`e2e` runs the same LUT_CORRECT through the C ABI (gpcx_lut_host) with
+pinned HOST buffers: H2D + kernels + D2H inside the timed region, on rank 0
+with all N GPUs bound in-process (the server's architecture).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LUT-correction Gpixel/s + matmul TFLOP/s at 1/2/4/8 B200 vs host CPU ref"
+ROWS = COLS = 32768
+SEED = 0x5EED
+MM = 4096  # config C2
+
+
+def splitmix64(x: int) -> int:
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+SEED_B = splitmix64(SEED)  # seed of matrix B (same derivation as the library's tests)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self._proc = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            self._proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9
+                          for i, v in enumerate(r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ dist ---
+
+class Dist:
+    def __init__(self, want: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if want != self.world and self.world != 1:
+            raise SystemExit(f"--gpus {want} but WORLD_SIZE={self.world}")
+        self.n = want if self.world == 1 else self.world
+        self.pg = None
+
+    def init(self, backend: str):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group("gloo")
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg is not None:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if self.pg.get_backend() == "nccl" else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+def band(rows: int, n: int, r: int) -> tuple[int, int]:
+    per = (rows + n - 1) // n
+    r0 = min(rows, r * per)
+    return r0, min(per, rows - r0)
+
+
+# ------------------------------------------------------------- B200 legs ---
+
+def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
+    import torch
+    from paper_1505_05655_b200 import device as D
+    dev = torch.device("cuda", d.local)
+    torch.cuda.set_device(dev)
+    r0, nr = band(ROWS, d.n, d.rank)
+    n = nr * COLS
+    img = D.synth_image(0, SEED, ROWS, COLS, r0, nr)
+    out = torch.empty_like(img)
+    hist = torch.zeros(65536, dtype=torch.int32, device=dev)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    stream = torch.cuda.current_stream()
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = {k: [] for k in ("h0", "h1", "a0", "a1")}
+
+    def step(record: bool):
+        if record:
+            ev["h0"].append(E()); ev["h0"][-1].record(stream)
+        D.lut_hist(img, hist, ws, stream)
+        if record:
+            ev["h1"].append(E()); ev["h1"][-1].record(stream)
+        if d.pg is not None:
+            d.pg.all_reduce(hist)
+        D.lut_from_hist(hist, mode, lut, stats, stream)
+        if record:
+            ev["a0"].append(E()); ev["a0"][-1].record(stream)
+        D.lut_apply(lut, img, out, stream)
+        if record:
+            ev["a1"].append(E()); ev["a1"][-1].record(stream)
+
+    for _ in range(warmup):
+        step(False)
+    torch.cuda.synchronize()
+    d.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = E(), E()
+    with Clocks(d.local) as clk:
+        t0.record(stream)
+        for _ in range(steps):
+            step(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    d.barrier()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    hist_ms = sum(a.elapsed_time(b) for a, b in zip(ev["h0"], ev["h1"])) / steps
+    apply_ms = sum(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"])) / steps
+    # correctness guard on the measured buffers (device digest vs nothing
+    # here; the oracle check of this exact band runs in the cpu leg).
+    dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
+    st = D.read_stats(stats)
+    return {"ms": ms, "hist_ms": hist_ms, "apply_ms": apply_ms, "band_px": n, "digest": dig,
+            "stats": st, "clocks": clk.summary()}
+
+
+def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int) -> dict:
+    """Rank 0, all N GPUs bound in-process: gpcx_lut_host with pinned host
+    buffers (H2D + kernels + D2H per step)."""
+    import ctypes as C
+    import torch
+    import paper_1505_05655_b200 as G
+    from paper_1505_05655_b200 import device as D
+    G.init(list(range(n_gpus)))
+    n = ROWS * COLS
+    p_in = G.lib.gpcx_pinned_alloc(n * 2)
+    p_out = G.lib.gpcx_pinned_alloc(n * 2)
+    try:
+        host_in = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p_in))
+        host_in[:] = D.synth_image(0, SEED, ROWS, COLS).cpu().numpy().view(np.uint16)
+        torch.cuda.empty_cache()
+        st = G.LutStats()
+        times = []
+        for i in range(warmup + steps):
+            t = time.perf_counter()
+            G.check(G.lib.gpcx_lut_host(2, mode, ROWS, COLS, C.c_void_p(p_in), None,
+                                        C.c_void_p(p_out), None, C.byref(st)))
+            if i >= warmup:
+                times.append(time.perf_counter() - t)
+    finally:
+        G.lib.gpcx_pinned_free(p_in)
+        G.lib.gpcx_pinned_free(p_out)
+        G.init([0])
+    tot = sum(times)
+    return {"value": n * steps / tot / 1e9, "ms_per_step": 1e3 * tot / steps,
+            "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": n * 2}
+
+
+def matmul_device_leg(steps: int, warmup: int) -> dict:
+    """Config C2: FP32 4096^3 on the SIMT reference-precision kernel; L2 is
+    flushed (256 MiB write) between steps, outside the GEMM events."""
+    import torch
+    from paper_1505_05655_b200 import device as D
+    A = D.synth_matrix(1, SEED, MM, MM)
+    B = D.synth_matrix(1, SEED_B, MM, MM)
+    Cm = torch.empty(MM, MM, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    times = []
+    for i in range(warmup + steps):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        D.matmul(0, A, B, Cm, None, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(a.elapsed_time(b))
+    ms = sum(times) / len(times)
+    flops = 2.0 * MM ** 3
+    return {"ms": ms, "tflops": flops / ms / 1e9, "C": Cm}
+
+
+def matmul_e2e_leg(steps: int) -> dict:
+    import ctypes as C
+    import paper_1505_05655_b200 as G
+    from paper_1505_05655_b200 import device as D
+    A = D.synth_matrix(1, SEED, MM, MM).cpu().numpy()
+    B = D.synth_matrix(1, SEED_B, MM, MM).cpu().numpy()
+    nb = MM * MM * 4
+    pa, pb, pc = (G.lib.gpcx_pinned_alloc(nb) for _ in range(3))
+    try:
+        np.ctypeslib.as_array((C.c_float * (MM * MM)).from_address(pa))[:] = A.ravel()
+        np.ctypeslib.as_array((C.c_float * (MM * MM)).from_address(pb))[:] = B.ravel()
+        times = []
+        for i in range(steps + 1):
+            t = time.perf_counter()
+            G.check(G.lib.gpcx_matmul_host(0, MM, MM, MM, C.c_void_p(pa), C.c_void_p(pb), C.c_void_p(pc)))
+            if i:
+                times.append(time.perf_counter() - t)
+    finally:
+        for p in (pa, pb, pc):
+            G.lib.gpcx_pinned_free(p)
+    s = sum(times) / len(times)
+    return {"value": 2.0 * MM ** 3 / s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 2 * nb,
+            "d2h_bytes_per_step": nb}
+
+
+# -------------------------------------------------------------- CPU legs ---
+
+def cpu_lut(mode: int, sample_rows: int = 4096, reps: int = 3) -> dict:
+    """The restated oracle (kind "port") on a row-band sample of the C3
+    scene with every host thread; returns Gpx/s and the band digest."""
+    from oracle import oracle as O
+    img = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS, 0, sample_rows)
+    times = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        O.lut_correct(img, mode)
+        times.append(time.perf_counter() - t)
+    px = sample_rows * COLS
+    return {"value": px / statistics.median(times) / 1e9, "unit": "Gpixel/s",
+            "cores": O.max_threads(), "kind": "port",
+            "sample": f"LUT_CORRECT equalize on a {sample_rows}x{COLS} band of the C3 scene, "
+                      f"median of {reps}, oracle/gpcx_oracle.c with {O.max_threads()} OpenMP threads",
+            "host": O.host_cpu()}
+
+
+def cpu_matmul(sample_rows: int = 64) -> dict:
+    from oracle import oracle as O
+    A = O.synth_matrix(O.MAT_UNIFORM32, SEED, MM, MM)
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(SEED), MM, MM)
+    rows = A[:sample_rows].copy()
+    t = time.perf_counter()
+    O.matmul_f32(rows, B)
+    s = time.perf_counter() - t
+    return {"value": 2.0 * sample_rows * MM * MM / s / 1e12, "unit": "TFLOP/s",
+            "cores": O.max_threads(), "kind": "port",
+            "sample": f"{sample_rows} rows of the C2 4096^3 FP32 product (f64 accumulate)"}
+
+
+# ----------------------------------------------------------------- main ---
+
+def traffic_from_profiles() -> dict:
+    p = ROOT / "profiles" / "traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def run_b200(args) -> None:
+    import torch
+    d = Dist(args.gpus)
+    d.init("nccl")
+    mode = 0
+    lut = lut_device_leg(d, args.steps, args.warmup, mode)
+    ms = d.max(lut["ms"])
+    apply_ms = d.max(lut["apply_ms"])
+    hist_ms = d.max(lut["hist_ms"])
+    mm = None
+    if d.rank == 0 and args.workload in ("all", "matmul"):
+        mm = matmul_device_leg(max(3, min(args.steps, 10)), 2)
+    d.barrier()
+    if d.rank != 0:
+        d.close()
+        return
+    d.close()
+    pk = peaks()
+    px_total = ROWS * COLS
+    value = px_total * args.steps / (ms / 1e3) / 1e9
+    band_px = lut["band_px"]
+    apply_ach = 4.0 * band_px / (apply_ms / 1e3) / 1e9
+    hist_ach = 2.0 * band_px / (hist_ms / 1e3) / 1e9
+    tr = traffic_from_profiles()
+    roof = {"bound": "hbm", "kernel": "lut::apply_kernel", "achieved": round(apply_ach, 1),
+            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(apply_ach / pk["hbm_gbs"], 4),
+            "traffic": tr.get("apply_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
+            "algorithmic_bytes_per_launch": 4 * band_px, "peak_source": pk["source"],
+            "kernels": {"hist_kernel+merge": {"achieved": round(hist_ach, 1),
+                                              "frac": round(hist_ach / pk["hbm_gbs"], 4),
+                                              "algorithmic_bytes": 2 * band_px,
+                                              "ms": round(hist_ms, 4)},
+                        "apply_kernel": {"ms": round(apply_ms, 4)},
+                        "step": {"achieved": round(6.0 * band_px / (ms / args.steps / 1e3) / 1e9, 1),
+                                 "frac": round(6.0 * band_px / (ms / args.steps / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                                 "algorithmic_bytes": 6 * band_px}}}
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "Gpixel/s", "n_gpus": d.n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic (ramp12 splitmix64 scene, generated on device)",
+            "config": {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene, row bands",
+                       "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
+                       "parallelism": f"row-band x{d.n}, NCCL all-reduce of the 65536-bin histogram",
+                       "l2": "inputs larger than L2 (2 GiB scene)"},
+            "roofline": roof, "gpu_launches": 4 * args.steps, "clocks": lut["clocks"]}
+    e2e = lut_e2e_leg(d.n, max(2, min(args.steps, 5)), 1, mode)
+    line["e2e"] = {"value": round(e2e["value"], 3), "unit": "Gpixel/s",
+                   "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                   "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                   "ms_per_step": round(e2e["ms_per_step"], 2),
+                   "path": "gpcx_lut_host (C ABI), pinned host buffers, all N GPUs in-process"}
+    if d.n == 1:
+        line["cpu_baseline"] = cpu_lut(mode)
+    if mm is not None:
+        mm_line = {"workload": "C2: MATMUL prec=f32 (SIMT), 4096^3", "value": round(mm["tflops"], 2),
+                   "unit": "TFLOP/s", "ms": round(mm["ms"], 3),
+                   "roofline": {"bound": "fp32-simt", "peak_note": "148 SMs x 128 FFMA x 2 x 1.965 GHz = 74.4 TFLOP/s nominal",
+                                "achieved": round(mm["tflops"], 2), "peak": 74.4,
+                                "frac": round(mm["tflops"] / 74.4, 4)},
+                   "l2": "flushed between steps (256 MiB write)"}
+        mm_line["e2e"] = matmul_e2e_leg(3)
+        if d.n == 1:
+            mm_line["cpu_baseline"] = cpu_matmul()
+        line["matmul"] = mm_line
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args) -> None:
+    """The reference arm: the restated CPU path on the host cores (there is
+    no reference LUT / matmul implementation to install)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    mode = 0
+    sample_rows = 2048
+    img = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS, 0, sample_rows)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        O.lut_correct(img, mode)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    px = sample_rows * COLS
+    value = px * len(times) / sum(times) / 1e9
+    sample = (f"LUT_CORRECT equalize on a {sample_rows}x{COLS} band of the C3 scene per step, "
+              f"oracle/gpcx_oracle.c (restatement; the reference has no LUT code)")
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "Gpixel/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene (sampled band)",
+                       "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "Gpixel/s", "cores": O.max_threads(),
+                             "kind": "port", "sample": sample, "host": O.host_cpu()},
+            "e2e": {"value": round(value, 4), "unit": "Gpixel/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=["all", "lut", "matmul"], default="all")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,380 @@
+// capi.cpp -- the extern "C" surface of include/gpcx.h.  Every entry point
+// converts C++ failures into a gpcx_status (1 + Errc ordinal) and a
+// thread-local message; nothing throws across the boundary.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "../../include/gpcx.h"
+#include "cuda_util.hpp"
+#include "host/executor.hpp"
+#include "host/registry.hpp"
+#include "host/runtime.hpp"
+#include "host/server.hpp"
+#include "host/task_spec.hpp"
+#include "kernels.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    g_last_error.clear();
+    return GPCX_OK;
+  } catch (const gpcx::Error& e) {
+    g_last_error = e.what();
+    return gpcx::to_status(e.code());
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return gpcx::to_status(gpcx::Errc::TaskFailed);
+  } catch (...) {
+    g_last_error = "unknown failure";
+    return gpcx::to_status(gpcx::Errc::TaskFailed);
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void copy_text(const std::string& text, char* out, uint64_t cap) {
+  if (out == nullptr || cap == 0) {
+    if (!text.empty()) gpcx::fail(gpcx::Errc::SizeMismatch, "text buffer too small");
+    return;
+  }
+  if (text.size() + 1 > cap)
+    gpcx::fail(gpcx::Errc::SizeMismatch, "text buffer holds " + std::to_string(cap) +
+                                             " bytes, need " + std::to_string(text.size() + 1));
+  std::memcpy(out, text.c_str(), text.size() + 1);
+}
+
+const char* nz(const char* s) { return s != nullptr ? s : ""; }
+
+void need_ws(void* ws, uint64_t have, uint64_t want) {
+  if (want > 0 && (ws == nullptr || have < want))
+    gpcx::fail(gpcx::Errc::SizeMismatch, "workspace holds " + std::to_string(have) +
+                                             " bytes, need " + std::to_string(want));
+}
+
+void need_u32(uint64_t n) {
+  if (n >= (1ull << 32)) gpcx::fail(gpcx::Errc::TooLarge, "more than 2^32-1 samples per call");
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpcx_abi_version(void) { return GPCX_ABI_VERSION; }
+
+int gpcx_init(int ndev, const int* devices) {
+  return guarded([&] {
+    std::vector<int> devs;
+    if (ndev < 0) gpcx::fail(gpcx::Errc::BadValue, "negative device count");
+    for (int i = 0; i < ndev; ++i) devs.push_back(devices != nullptr ? devices[i] : i);
+    gpcx::rt::Runtime::get().init(devs);
+  });
+}
+
+int gpcx_shutdown(void) {
+  return guarded([] {
+    gpcx::rt::Runtime::get().shutdown();
+    gpcx::rt::pinned_trim();
+  });
+}
+
+int gpcx_device_count(int* count) {
+  return guarded([&] { *count = gpcx::rt::Runtime::get().ndev(); });
+}
+
+const char* gpcx_last_error(void) { return g_last_error.c_str(); }
+
+const char* gpcx_status_name(int status) {
+  if (status == GPCX_OK) return "OK";
+  if (status < 1 || status > gpcx::kErrcCount) return "Unknown";
+  return gpcx::errc_name(static_cast<gpcx::Errc>(status - 1));
+}
+
+const char* gpcx_response_code(int status) {
+  static thread_local std::string code;
+  if (status == GPCX_OK) return "OK";
+  if (status < 1 || status > gpcx::kErrcCount) return "TASK_FAILED";
+  code = gpcx::response_code(static_cast<gpcx::Errc>(status - 1));
+  return code.c_str();
+}
+
+int gpcx_payload_len(const char* flag, const char* params, uint64_t* len) {
+  return guarded([&] {
+    const auto f = gpcx::task::flag_of(nz(flag));
+    *len = gpcx::task::payload_len(f, gpcx::wire::ParamMap::parse(nz(params)));
+  });
+}
+
+int gpcx_output_len(const char* flag, const char* params, uint64_t* len) {
+  return guarded([&] {
+    const auto f = gpcx::task::flag_of(nz(flag));
+    *len = gpcx::task::output_len(f, gpcx::wire::ParamMap::parse(nz(params)));
+  });
+}
+
+int gpcx_required_params(const char* flag, char* out, uint64_t cap) {
+  return guarded([&] {
+    std::string text;
+    for (const std::string& k : gpcx::task::required_params(gpcx::task::flag_of(nz(flag)))) {
+      if (!text.empty()) text += ',';
+      text += k;
+    }
+    copy_text(text, out, cap);
+  });
+}
+
+int gpcx_flags(char* out, uint64_t cap) {
+  return guarded([&] {
+    std::string text;
+    for (const auto f : gpcx::task::all_flags()) {
+      if (!text.empty()) text += ',';
+      text += gpcx::task::flag_name(f);
+    }
+    copy_text(text, out, cap);
+  });
+}
+
+int gpcx_run(const char* flag, const char* params, const void* in, uint64_t in_len, void* out,
+             uint64_t out_cap, uint64_t* out_len, char* result_params,
+             uint64_t result_params_cap) {
+  return guarded([&] {
+    const auto f = gpcx::task::flag_of(nz(flag));
+    const auto p = gpcx::wire::ParamMap::parse(nz(params));
+    const uint64_t want = gpcx::task::output_len(f, p);
+    if (out_cap < want)
+      gpcx::fail(gpcx::Errc::SizeMismatch, "output buffer holds " + std::to_string(out_cap) +
+                                               " bytes, need " + std::to_string(want));
+    if (in_len > 0 && in == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null payload");
+    const auto result = gpcx::exec::execute(
+        f, p, std::span<const std::uint8_t>(static_cast<const std::uint8_t*>(in), in_len),
+        std::span<std::uint8_t>(static_cast<std::uint8_t*>(out), want));
+    if (out_len != nullptr) *out_len = want;
+    if (result_params != nullptr) copy_text(result.serialize(), result_params, result_params_cap);
+  });
+}
+
+int gpcx_lut_host(int op, int mode, uint64_t rows, uint64_t cols, const uint16_t* img,
+                  const uint16_t* lut_in, uint16_t* out, uint16_t* lut_out,
+                  gpcx_lut_stats* stats) {
+  return guarded([&] {
+    using gpcx::task::Flag;
+    const Flag f = op == GPCX_OP_LUT_GEN     ? Flag::LutGen
+                   : op == GPCX_OP_LUT_APPLY ? Flag::LutApply
+                   : op == GPCX_OP_LUT_CORRECT
+                       ? Flag::LutCorrect
+                       : (gpcx::fail(gpcx::Errc::BadValue, "op " + std::to_string(op)), Flag::LutGen);
+    if (rows == 0 || cols == 0) gpcx::fail(gpcx::Errc::BadValue, "rows and cols must be positive");
+    if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    if (img == nullptr || out == nullptr || (f == Flag::LutApply && lut_in == nullptr))
+      gpcx::fail(gpcx::Errc::BadValue, "null buffer");
+    need_u32(rows * cols);
+    gpcx::task::LutParams p;
+    p.rows = rows;
+    p.cols = cols;
+    p.mode = mode;
+    const gpcx_lut_stats st = gpcx::exec::lut_host(f, p, img, lut_in, out, lut_out);
+    if (stats != nullptr) *stats = st;
+  });
+}
+
+int gpcx_matmul_host(int prec, uint64_t m, uint64_t n, uint64_t k, const float* A,
+                     const float* B, float* C) {
+  return guarded([&] {
+    if (m == 0 || n == 0 || k == 0) gpcx::fail(gpcx::Errc::BadValue, "dimensions must be positive");
+    if (prec != GPCX_PREC_F32 && prec != GPCX_PREC_TF32 && prec != GPCX_PREC_BF16)
+      gpcx::fail(gpcx::Errc::BadValue, "prec " + std::to_string(prec));
+    gpcx::task::MatmulParams p;
+    p.m = m;
+    p.n = n;
+    p.k = k;
+    p.prec = prec;
+    gpcx::exec::matmul_host(p, A, B, C);
+  });
+}
+
+void* gpcx_pinned_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes == 0 ? 1 : bytes) != cudaSuccess) {
+    cudaGetLastError();
+    g_last_error = "cudaMallocHost failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void gpcx_pinned_free(void* ptr) {
+  if (ptr != nullptr) cudaFreeHost(ptr);
+}
+
+int gpcx_lut_workspace_size(uint64_t n, uint64_t* bytes) {
+  return guarded([&] {
+    need_u32(n);
+    *bytes = gpcx::lut::workspace_bytes();
+  });
+}
+
+int gpcx_lut_hist_device(const uint16_t* img, uint64_t n, uint32_t* hist, void* ws,
+                         uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    gpcx::lut::launch_hist(img, n, hist, ws, as_stream(stream));
+  });
+}
+
+int gpcx_lut_from_hist_device(const uint32_t* hist, int mode, uint16_t* lut,
+                              gpcx_lut_stats* stats, void* stream) {
+  return guarded([&] {
+    if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    gpcx::lut::launch_from_hist(hist, mode, lut, stats, as_stream(stream));
+  });
+}
+
+int gpcx_lut_minmax_device(const uint16_t* img, uint64_t n, gpcx_lut_stats* stats, void* ws,
+                           uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    gpcx::lut::launch_minmax(img, n, stats, ws, as_stream(stream));
+  });
+}
+
+int gpcx_lut_from_minmax_device(const gpcx_lut_stats* stats, uint16_t* lut, void* stream) {
+  return guarded([&] { gpcx::lut::launch_from_minmax(stats, lut, as_stream(stream)); });
+}
+
+int gpcx_lut_gen_device(const uint16_t* img, uint64_t n, int mode, uint16_t* lut,
+                        gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    const cudaStream_t s = as_stream(stream);
+    if (mode == GPCX_LUT_EQUALIZE) {
+      gpcx::lut::launch_hist(img, n, gpcx::lut::ws_hist(ws), ws, s);
+      gpcx::lut::launch_from_hist(gpcx::lut::ws_hist(ws), mode, lut, stats, s);
+    } else if (mode == GPCX_LUT_STRETCH) {
+      gpcx::lut::launch_minmax(img, n, stats, ws, s);
+      gpcx::lut::launch_from_minmax(stats, lut, s);
+    } else {
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    }
+  });
+}
+
+int gpcx_lut_apply_device(const uint16_t* lut, const uint16_t* in, uint16_t* out, uint64_t n,
+                          void* stream) {
+  return guarded([&] { gpcx::lut::launch_apply(lut, in, out, n, as_stream(stream)); });
+}
+
+int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n, int mode,
+                            uint16_t* lut, gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
+                            void* stream) {
+  const int rc = gpcx_lut_gen_device(in, n, mode, lut, stats, ws, ws_bytes, stream);
+  if (rc != GPCX_OK) return rc;
+  return gpcx_lut_apply_device(lut, in, out, n, stream);
+}
+
+int gpcx_matmul_workspace_size(int prec, uint64_t m, uint64_t n, uint64_t k, uint64_t* bytes) {
+  return guarded([&] {
+    *bytes = prec == GPCX_PREC_F32 ? 0 : gpcx::gemm::tc_workspace_bytes(prec, m, n, k);
+  });
+}
+
+int gpcx_matmul_device(int prec, uint64_t m, uint64_t n, uint64_t k, const float* A,
+                       uint64_t lda, const float* B, uint64_t ldb, float* C, uint64_t ldc,
+                       void* ws, uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    if (lda < k || ldb < n || ldc < n)
+      gpcx::fail(gpcx::Errc::BadValue, "leading dimension smaller than the row length");
+    if (prec == GPCX_PREC_F32) {
+      gpcx::gemm::launch_sgemm(m, n, k, A, lda, B, ldb, C, ldc, as_stream(stream));
+    } else if (prec == GPCX_PREC_TF32 || prec == GPCX_PREC_BF16) {
+      need_ws(ws, ws_bytes, gpcx::gemm::tc_workspace_bytes(prec, m, n, k));
+      gpcx::gemm::launch_tc(prec, m, n, k, A, lda, B, ldb, C, ldc, ws, as_stream(stream));
+    } else {
+      gpcx::fail(gpcx::Errc::BadValue, "prec " + std::to_string(prec));
+    }
+  });
+}
+
+int gpcx_synth_image_device(int kind, uint64_t seed, uint64_t rows, uint64_t cols, uint64_t row0,
+                            uint64_t nrows, uint16_t* out, void* stream) {
+  return guarded([&] {
+    if (kind != GPCX_IMG_RAMP12 && kind != GPCX_IMG_UNIFORM16)
+      gpcx::fail(gpcx::Errc::BadValue, "image kind " + std::to_string(kind));
+    gpcx::synth::launch_image(kind, seed, rows, cols, row0, nrows, out, as_stream(stream));
+  });
+}
+
+int gpcx_synth_matrix_device(int kind, uint64_t seed, uint64_t rows, uint64_t cols,
+                             uint64_t row0, uint64_t nrows, float* out, void* stream) {
+  return guarded([&] {
+    if (kind != GPCX_MAT_EXACT8 && kind != GPCX_MAT_UNIFORM32)
+      gpcx::fail(gpcx::Errc::BadValue, "matrix kind " + std::to_string(kind));
+    gpcx::synth::launch_matrix(kind, seed, rows, cols, row0, nrows, out, as_stream(stream));
+  });
+}
+
+int gpcx_digest_u16_device(const uint16_t* v, uint64_t n, uint64_t index0, uint64_t* digest,
+                           void* stream) {
+  return guarded([&] { gpcx::synth::launch_digest(v, n, index0, digest, as_stream(stream)); });
+}
+
+struct gpcx_server_handle {
+  gpcx::task::TaskRegistry registry;
+  std::unique_ptr<gpcx::srv::Server> server;
+};
+
+int gpcx_server_start(const char* bind_addr, uint16_t port, int max_tasks, int idle_timeout_ms,
+                      void** handle, uint16_t* bound_port) {
+  return guarded([&] {
+    auto h = std::make_unique<gpcx_server_handle>();
+    h->registry = gpcx::task::make_b200_registry();
+    gpcx::srv::ServerConfig cfg;
+    cfg.bind_addr = bind_addr != nullptr ? bind_addr : "0.0.0.0";
+    cfg.port = port;
+    cfg.max_tasks = max_tasks;
+    if (idle_timeout_ms > 0) cfg.idle_timeout = std::chrono::milliseconds(idle_timeout_ms);
+    const char* quiet = std::getenv("GPCX_QUIET");
+    cfg.log = !(quiet != nullptr && quiet[0] == '1');
+    h->server = std::make_unique<gpcx::srv::Server>(cfg, h->registry);
+    h->server->start();
+    if (bound_port != nullptr) *bound_port = h->server->port();
+    *handle = h.release();
+  });
+}
+
+int gpcx_server_stop(void* handle) {
+  return guarded([&] {
+    auto* h = static_cast<gpcx_server_handle*>(handle);
+    if (h == nullptr) return;
+    h->server->stop();
+    delete h;
+  });
+}
+
+int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp, uint64_t resp_cap,
+                        uint64_t* resp_len) {
+  return guarded([&] {
+    static const gpcx::task::TaskRegistry* registry =
+        new gpcx::task::TaskRegistry(gpcx::task::make_b200_registry());
+    gpcx::wire::MemoryStream stream(std::vector<std::uint8_t>(req, req + req_len));
+    gpcx::srv::handle_connection(stream, *registry);
+    const auto& bytes = stream.written();
+    if (resp_len != nullptr) *resp_len = bytes.size();
+    if (bytes.size() > resp_cap)
+      gpcx::fail(gpcx::Errc::SizeMismatch, "response buffer holds " + std::to_string(resp_cap) +
+                                               " bytes, need " + std::to_string(bytes.size()));
+    if (!bytes.empty()) std::memcpy(resp, bytes.data(), bytes.size());
+  });
+}
+
+}  // extern "C"

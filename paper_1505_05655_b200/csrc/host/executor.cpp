@@ -1,0 +1,259 @@
+// executor.cpp -- see executor.hpp.
+//
+// Planner.  A request runs on one device (round robin over
+// the bound devices, i.e. replicas for many small requests) unless it is
+// large and several devices are bound; then:
+//   LUT_*   : row bands of ceil(rows/G) rows.  Equalize needs the global
+//             histogram: each device histograms its band, the 256 KiB
+//             partial histograms are summed (one exchange step), every
+//             device builds the identical LUT and applies it to its band,
+//             and each band is DMA'd straight into its disjoint slice of the
+//             host response buffer -- that D2H is the gather.
+//   MATMUL  : block rows of A and C, B replicated; tile / K order do not
+//             depend on G, so C is bitwise identical for any device count
+//             (the analogue of acceptance.cpp:278-315's worker invariance).
+#include "executor.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <future>
+#include <string>
+#include <vector>
+
+#include "../cuda_util.hpp"
+#include "../kernels.hpp"
+#include "runtime.hpp"
+
+namespace gpcx::exec {
+
+namespace {
+
+using task::Flag;
+
+struct Band {
+  int dev_index;
+  std::uint64_t row0, nrows;
+};
+
+std::vector<Band> plan_bands(std::uint64_t rows, std::uint64_t work, std::uint64_t threshold) {
+  rt::Runtime& R = rt::Runtime::get();
+  const int ndev = R.ndev();
+  if (ndev <= 1 || work < threshold || rows < 2) return {Band{R.pick_device_index(), 0, rows}};
+  const std::uint64_t g = std::min<std::uint64_t>(static_cast<std::uint64_t>(ndev), rows);
+  const std::uint64_t per = (rows + g - 1) / g;
+  std::vector<Band> bands;
+  for (std::uint64_t i = 0; i < g; ++i) {
+    const std::uint64_t r0 = i * per;
+    if (r0 >= rows) break;
+    bands.push_back(Band{static_cast<int>(i), r0, std::min(per, rows - r0)});
+  }
+  return bands;
+}
+
+// Runs fn(i) for every band concurrently (one host thread per device so
+// pageable staging of different bands overlaps); rethrows the lowest-index
+// failure, like gpc::par::parallel_for (parexec.hpp:55-75).
+template <class Fn>
+void for_each_band(std::size_t count, Fn&& fn) {
+  if (count == 1) {
+    fn(0);
+    return;
+  }
+  std::vector<std::future<void>> futs;
+  futs.reserve(count);
+  for (std::size_t i = 0; i < count; ++i)
+    futs.push_back(std::async(std::launch::async, [&fn, i] { fn(i); }));
+  std::exception_ptr first;
+  for (auto& f : futs) {
+    try {
+      f.get();
+    } catch (...) {
+      if (!first) first = std::current_exception();
+    }
+  }
+  if (first) std::rethrow_exception(first);
+}
+
+
+}  // namespace
+
+// LUT_GEN / LUT_CORRECT / LUT_APPLY on host buffers.  `img` is the image,
+// `lut_in` the LUT for LUT_APPLY, `out` the image (CORRECT / APPLY) or the
+// LUT (GEN); `lut_out` optionally receives the LUT of CORRECT.
+gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t* img_in,
+                        const std::uint16_t* lut_in, std::uint16_t* out_px,
+                        std::uint16_t* lut_out) {
+  const std::uint64_t n = p.pixels();
+  const auto* img = reinterpret_cast<const std::uint8_t*>(img_in);
+  auto* outb = reinterpret_cast<std::uint8_t*>(out_px);
+  const std::vector<Band> bands = plan_bands(p.rows, n, kShardMinPixels);
+  const std::size_t G = bands.size();
+  rt::Runtime& R = rt::Runtime::get();
+
+  std::vector<rt::SlotLease> leases;
+  leases.reserve(G);
+  for (const Band& b : bands) leases.push_back(R.acquire(b.dev_index));
+
+  const bool need_apply = flag != Flag::LutGen;
+  const bool equalize = p.mode == GPCX_LUT_EQUALIZE;
+
+  // Phase 1: stage each band into HBM; local statistics.
+  std::vector<std::vector<std::uint32_t>> hists(G);
+  std::vector<gpcx_lut_stats> local(G);
+  for_each_band(G, [&](std::size_t i) {
+    rt::Slot& s = *leases[i];
+    rt::use_device(s.device);
+    const Band& b = bands[i];
+    const std::uint64_t bn = b.nrows * p.cols;
+    s.a.ensure(bn * 2);
+    rt::h2d(s, s.a.ptr, img + b.row0 * p.cols * 2, bn * 2);
+    if (flag == Flag::LutApply) {
+      rt::h2d(s, s.d_lut(), lut_in, task::kLutBytes);
+      return;
+    }
+    if (G == 1) return;  // single device: generate in phase 2 directly
+    if (equalize) {
+      lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream);
+      hists[i].resize(65536);
+      rt::d2h(s, hists[i].data(), s.d_hist(), 65536 * 4);
+    } else {
+      lut::launch_minmax(s.a.as<std::uint16_t>(), bn, s.d_stats(), s.lut_ws.ptr, s.stream);
+      rt::d2h(s, &local[i], s.d_stats(), sizeof(gpcx_lut_stats));
+    }
+  });
+
+  // Exchange: combine the band statistics (integer sums / min-max, so the
+  // result is independent of G).
+  std::vector<std::uint32_t> global_hist;
+  gpcx_lut_stats global_mm{n, 0xFFFFFFFFu, 0, 0};
+  if (G > 1 && flag != Flag::LutApply) {
+    if (equalize) {
+      global_hist.assign(65536, 0);
+      for (const auto& h : hists)
+        for (int v = 0; v < 65536; ++v) global_hist[v] += h[v];
+    } else {
+      for (const auto& st : local) {
+        global_mm.lo = std::min(global_mm.lo, st.lo);
+        global_mm.hi = std::max(global_mm.hi, st.hi);
+      }
+    }
+  }
+
+  // Phase 2: LUT on every device, apply, DMA each band into its slice.
+  std::vector<gpcx_lut_stats> stats(G);
+  for_each_band(G, [&](std::size_t i) {
+    rt::Slot& s = *leases[i];
+    rt::use_device(s.device);
+    const Band& b = bands[i];
+    const std::uint64_t bn = b.nrows * p.cols;
+    auto* dimg = s.a.as<std::uint16_t>();
+    if (flag != Flag::LutApply) {
+      if (G == 1) {
+        if (equalize) {
+          lut::launch_hist(dimg, bn, s.d_hist(), s.lut_ws.ptr, s.stream);
+          lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.stream);
+        } else {
+          lut::launch_minmax(dimg, bn, s.d_stats(), s.lut_ws.ptr, s.stream);
+          lut::launch_from_minmax(s.d_stats(), s.d_lut(), s.stream);
+        }
+      } else if (equalize) {
+        GPCX_CUDA(cudaMemcpyAsync(s.d_hist(), global_hist.data(), 65536 * 4,
+                                  cudaMemcpyHostToDevice, s.stream));
+        lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.stream);
+      } else {
+        GPCX_CUDA(cudaMemcpyAsync(s.d_stats(), &global_mm, sizeof(global_mm),
+                                  cudaMemcpyHostToDevice, s.stream));
+        lut::launch_from_minmax(s.d_stats(), s.d_lut(), s.stream);
+      }
+      GPCX_CUDA(cudaMemcpyAsync(s.h_stats(), s.d_stats(), sizeof(gpcx_lut_stats),
+                                cudaMemcpyDeviceToHost, s.stream));
+    }
+    if (need_apply) {
+      lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
+      rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
+      if (lut_out != nullptr && i == 0)
+        GPCX_CUDA(cudaMemcpy(lut_out, s.d_lut(), task::kLutBytes, cudaMemcpyDeviceToHost));
+    } else if (i == 0) {
+      rt::d2h(s, outb, s.d_lut(), task::kLutBytes);
+    } else {
+      GPCX_CUDA(cudaStreamSynchronize(s.stream));
+    }
+    if (flag != Flag::LutApply) stats[i] = *s.h_stats();
+  });
+
+  return flag == Flag::LutApply ? gpcx_lut_stats{n, 0, 0, 0} : stats[0];
+}
+
+void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* Cout) {
+  auto* outb = reinterpret_cast<std::uint8_t*>(Cout);
+  const std::vector<Band> bands = plan_bands(p.m, 2 * p.m * p.n * p.k, kShardMinFlops);
+  const std::size_t G = bands.size();
+  rt::Runtime& R = rt::Runtime::get();
+  std::vector<rt::SlotLease> leases;
+  leases.reserve(G);
+  for (const Band& b : bands) leases.push_back(R.acquire(b.dev_index));
+
+  for_each_band(G, [&](std::size_t i) {
+    rt::Slot& s = *leases[i];
+    rt::use_device(s.device);
+    const Band& b = bands[i];
+    s.a.ensure(std::max<std::uint64_t>(b.nrows * p.k * 4, 4));
+    s.b.ensure(std::max<std::uint64_t>(p.k * p.n * 4, 4));
+    s.c.ensure(std::max<std::uint64_t>(b.nrows * p.n * 4, 4));
+    rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
+    rt::h2d(s, s.b.ptr, B, p.k * p.n * 4);
+    if (p.prec == GPCX_PREC_F32) {
+      gemm::launch_sgemm(b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,
+                         s.c.as<float>(), p.n, s.stream);
+    } else {
+      s.mm_ws.ensure(gemm::tc_workspace_bytes(p.prec, b.nrows, p.n, p.k));
+      gemm::launch_tc(p.prec, b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,
+                      s.c.as<float>(), p.n, s.mm_ws.ptr, s.stream);
+    }
+    rt::d2h(s, outb + b.row0 * p.n * 4, s.c.ptr, b.nrows * p.n * 4);
+  });
+
+}
+
+wire::ParamMap execute(Flag flag, const wire::ParamMap& params,
+                       std::span<const std::uint8_t> in, std::span<std::uint8_t> out) {
+  const std::uint64_t want_in = task::payload_len(flag, params);
+  if (in.size() != want_in)
+    fail(Errc::PayloadMismatch,
+         "payload is " + std::to_string(in.size()) + " bytes, want " + std::to_string(want_in));
+  const std::uint64_t want_out = task::output_len(flag, params);
+  if (out.size() < want_out)
+    fail(Errc::SizeMismatch, "output buffer holds " + std::to_string(out.size()) +
+                                 " bytes, need " + std::to_string(want_out));
+  wire::ParamMap result;
+  if (flag == Flag::Matmul) {
+    const task::MatmulParams p = task::parse_matmul(params);
+    const auto* A = reinterpret_cast<const float*>(in.data());
+    matmul_host(p, A, A + p.m * p.k, reinterpret_cast<float*>(out.data()));
+    result.set("m", p.m);
+    result.set("n", p.n);
+    result.set("k", p.k);
+    result.set("prec", task::prec_name(p.prec));
+    return result;
+  }
+  const task::LutParams p = task::parse_lut(flag, params);
+  const auto* words = reinterpret_cast<const std::uint16_t*>(in.data());
+  const bool apply_only = flag == Flag::LutApply;
+  const gpcx_lut_stats st = lut_host(flag, p, apply_only ? words + 65536 : words,
+                                     apply_only ? words : nullptr,
+                                     reinterpret_cast<std::uint16_t*>(out.data()), nullptr);
+  result.set("rows", p.rows);
+  result.set("cols", p.cols);
+  if (!apply_only) {
+    result.set("mode", task::mode_name(p.mode));
+    result.set("lo", static_cast<std::uint64_t>(st.lo));
+    result.set("hi", static_cast<std::uint64_t>(st.hi));
+    if (p.mode == GPCX_LUT_EQUALIZE) result.set("cdf_min", st.cdf_min);
+  }
+  return result;
+}
+
+}  // namespace gpcx::exec

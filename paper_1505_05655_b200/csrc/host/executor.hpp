@@ -1,0 +1,34 @@
+// executor.hpp -- runs one GPU task request: the body behind gpcx_run and
+// the server's handlers.  The reference equivalent is a TaskDescriptor
+// handler: params -> decode -> kernel -> encode -> result params
+// (proj/src/tasks.cpp:13-35); here it is params -> H2D (async, per-request
+// stream) -> sm_100a kernels -> D2H, with the multi-GPU shard/gather planner
+// deciding how many devices take part.
+#pragma once
+
+#include <cstdint>
+#include <span>
+
+#include "task_spec.hpp"
+#include "wire.hpp"
+
+namespace gpcx::exec {
+
+// `in` / `out` are host memory (pinned or pageable).  out.size() must be at
+// least task::output_len().  Returns the result params (without bytes=).
+wire::ParamMap execute(task::Flag flag, const wire::ParamMap& params,
+                       std::span<const std::uint8_t> in, std::span<std::uint8_t> out);
+
+// The same, on typed host buffers and without the wire's 1 GiB cap (the
+// in-process entry points gpcx_lut_host / gpcx_matmul_host).
+gpcx_lut_stats lut_host(task::Flag flag, const task::LutParams& p, const std::uint16_t* img,
+                        const std::uint16_t* lut_in, std::uint16_t* out,
+                        std::uint16_t* lut_out);
+void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* C);
+
+// Work size (pixels or output rows) below which a request stays on one
+// device even when several are bound.
+inline constexpr std::uint64_t kShardMinPixels = 1ull << 24;
+inline constexpr std::uint64_t kShardMinFlops = 1ull << 36;
+
+}  // namespace gpcx::exec

@@ -1,0 +1,291 @@
+// runtime.cpp -- see runtime.hpp.
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "../cuda_util.hpp"
+#include "../kernels.hpp"
+
+namespace gpcx::rt {
+
+void use_device(int device) { GPCX_CUDA(cudaSetDevice(device)); }
+
+void DeviceBuf::ensure(std::uint64_t bytes, bool zero) {
+  if (bytes <= cap && ptr != nullptr) return;
+  release();
+  const std::uint64_t want = std::max<std::uint64_t>(bytes, 256);
+  GPCX_CUDA(cudaMalloc(&ptr, want));
+  cap = want;
+  if (zero) GPCX_CUDA(cudaMemset(ptr, 0, want));
+}
+
+void DeviceBuf::release() {
+  if (ptr != nullptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+
+void PinnedBuf::ensure(std::uint64_t bytes) {
+  if (bytes <= cap && ptr != nullptr) return;
+  release();
+  GPCX_CUDA(cudaMallocHost(&ptr, std::max<std::uint64_t>(bytes, 256)));
+  cap = std::max<std::uint64_t>(bytes, 256);
+}
+
+void PinnedBuf::release() {
+  if (ptr != nullptr) cudaFreeHost(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+
+Slot::~Slot() {
+  cudaSetDevice(device);
+  if (stream != nullptr) cudaStreamSynchronize(stream);
+  a.release();
+  b.release();
+  c.release();
+  lut_ws.release();
+  mm_ws.release();
+  small.release();
+  stage[0].release();
+  stage[1].release();
+  h_small.release();
+  for (cudaEvent_t& e : chunk_done)
+    if (e != nullptr) cudaEventDestroy(e);
+  if (stream != nullptr) cudaStreamDestroy(stream);
+}
+
+SlotLease::~SlotLease() {
+  if (slot_ != nullptr) rt_->release(slot_);
+}
+
+Runtime& Runtime::get() {
+  static Runtime* rt = new Runtime();  // never destroyed: outlives static teardown
+  return *rt;
+}
+
+void Runtime::init(const std::vector<int>& devices) {
+  std::lock_guard<std::mutex> lock(mu_);
+  std::vector<int> want = devices;
+  if (want.empty()) {
+    int count = 0;
+    GPCX_CUDA(cudaGetDeviceCount(&count));
+    for (int i = 0; i < count; ++i) want.push_back(i);
+  }
+  if (want.empty()) fail(Errc::TaskFailed, "no CUDA device available");
+  std::vector<int> have;
+  for (const Pool& p : pools_) have.push_back(p.device);
+  if (inited_ && have == want) return;
+  pools_.clear();
+  for (int d : want) {
+    int count = 0;
+    GPCX_CUDA(cudaGetDeviceCount(&count));
+    if (d < 0 || d >= count) fail(Errc::BadValue, "device " + std::to_string(d) + " not present");
+    pools_.push_back(Pool{d, {}, {}});
+  }
+  inited_ = true;
+}
+
+void Runtime::shutdown() {
+  std::lock_guard<std::mutex> lock(mu_);
+  pools_.clear();
+  inited_ = false;
+}
+
+void Runtime::ensure_init_locked() {
+  if (inited_) return;
+  int count = 0;
+  GPCX_CUDA(cudaGetDeviceCount(&count));
+  if (count <= 0) fail(Errc::TaskFailed, "no CUDA device available");
+  for (int i = 0; i < count; ++i) pools_.push_back(Pool{i, {}, {}});
+  inited_ = true;
+}
+
+std::vector<int> Runtime::devices() {
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  std::vector<int> out;
+  for (const Pool& p : pools_) out.push_back(p.device);
+  return out;
+}
+
+int Runtime::ndev() { return static_cast<int>(devices().size()); }
+
+int Runtime::pick_device_index() {
+  const int n = ndev();
+  return static_cast<int>(rr_.fetch_add(1) % static_cast<unsigned>(n));
+}
+
+SlotLease Runtime::acquire(int device_index) {
+  std::unique_lock<std::mutex> lock(mu_);
+  ensure_init_locked();
+  Pool& pool = pools_.at(static_cast<std::size_t>(device_index));
+  if (!pool.free.empty()) {
+    Slot* s = pool.free.back();
+    pool.free.pop_back();
+    lock.unlock();
+    use_device(s->device);
+    return SlotLease(this, s);
+  }
+  const int device = pool.device;
+  lock.unlock();
+  auto slot = std::make_unique<Slot>();
+  slot->device = device;
+  use_device(device);
+  GPCX_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : slot->chunk_done)
+    GPCX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  slot->small.ensure(131072 + 256 + 65536 * 4);
+  slot->h_small.ensure(256);
+  slot->lut_ws.ensure(lut::workspace_bytes(), /*zero=*/true);
+  Slot* raw = slot.get();
+  lock.lock();
+  pool.all.push_back(std::move(slot));
+  return SlotLease(this, raw);
+}
+
+void Runtime::release(Slot* slot) {
+  std::lock_guard<std::mutex> lock(mu_);
+  for (Pool& p : pools_) {
+    if (p.device != slot->device) continue;
+    for (auto& owned : p.all) {
+      if (owned.get() == slot) {
+        p.free.push_back(slot);
+        return;
+      }
+    }
+  }
+  // Pool was rebuilt while the slot was leased: the unique_ptr that owned it
+  // is gone already only if shutdown raced a request, which the C ABI
+  // documents as unsupported; nothing to return it to.
+}
+
+namespace {
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<std::uint64_t, void*>> idle;  // (capacity, ptr)
+  std::uint64_t idle_bytes = 0;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool();
+  return *p;
+}
+constexpr std::uint64_t kPinnedIdleCap = 8ull << 30;
+}  // namespace
+
+PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
+  if (this != &o) {
+    this->~PinnedLease();
+    ptr_ = o.ptr_;
+    cap_ = o.cap_;
+    o.ptr_ = nullptr;
+  }
+  return *this;
+}
+
+PinnedLease::~PinnedLease() {
+  if (ptr_ == nullptr) return;
+  PinnedPool& pool = pinned_pool();
+  std::lock_guard<std::mutex> lock(pool.mu);
+  if (pool.idle_bytes + cap_ > kPinnedIdleCap) {
+    cudaFreeHost(ptr_);
+  } else {
+    pool.idle.emplace_back(cap_, ptr_);
+    pool.idle_bytes += cap_;
+  }
+  ptr_ = nullptr;
+}
+
+PinnedLease pinned_acquire(std::uint64_t bytes) {
+  std::uint64_t cls = 4096;
+  while (cls < bytes) cls <<= 1;
+  PinnedPool& pool = pinned_pool();
+  {
+    std::lock_guard<std::mutex> lock(pool.mu);
+    for (std::size_t i = 0; i < pool.idle.size(); ++i) {
+      if (pool.idle[i].first == cls) {
+        void* p = pool.idle[i].second;
+        pool.idle.erase(pool.idle.begin() + static_cast<std::ptrdiff_t>(i));
+        pool.idle_bytes -= cls;
+        return PinnedLease(p, cls);
+      }
+    }
+  }
+  void* p = nullptr;
+  GPCX_CUDA(cudaHostAlloc(&p, cls, cudaHostAllocPortable));
+  return PinnedLease(p, cls);
+}
+
+void pinned_trim() {
+  PinnedPool& pool = pinned_pool();
+  std::lock_guard<std::mutex> lock(pool.mu);
+  for (auto& e : pool.idle) cudaFreeHost(e.second);
+  pool.idle.clear();
+  pool.idle_bytes = 0;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
+void h2d(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
+  if (bytes == 0) return;
+  if (is_pinned(src)) {
+    GPCX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s.stream));
+    return;
+  }
+  const std::uint64_t chunk = std::min<std::uint64_t>(kStageChunk, bytes);
+  s.stage[0].ensure(chunk);
+  s.stage[1].ensure(chunk);
+  const auto* in = static_cast<const unsigned char*>(src);
+  auto* out = static_cast<unsigned char*>(dst);
+  std::uint64_t off = 0;
+  for (int i = 0; off < bytes; ++i, off += chunk) {
+    const std::uint64_t len = std::min(chunk, bytes - off);
+    PinnedBuf& st = s.stage[i & 1];
+    GPCX_CUDA(cudaEventSynchronize(s.chunk_done[i & 1]));  // previous DMA out of st
+    std::memcpy(st.ptr, in + off, len);
+    GPCX_CUDA(cudaMemcpyAsync(out + off, st.ptr, len, cudaMemcpyHostToDevice, s.stream));
+    GPCX_CUDA(cudaEventRecord(s.chunk_done[i & 1], s.stream));
+  }
+}
+
+void d2h(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
+  if (bytes == 0) {
+    GPCX_CUDA(cudaStreamSynchronize(s.stream));
+    return;
+  }
+  if (is_pinned(dst)) {
+    GPCX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s.stream));
+    GPCX_CUDA(cudaStreamSynchronize(s.stream));
+    return;
+  }
+  const std::uint64_t chunk = std::min<std::uint64_t>(kStageChunk, bytes);
+  s.stage[0].ensure(chunk);
+  s.stage[1].ensure(chunk);
+  const auto* in = static_cast<const unsigned char*>(src);
+  auto* out = static_cast<unsigned char*>(dst);
+  const std::uint64_t nchunks = (bytes + chunk - 1) / chunk;
+  auto issue = [&](std::uint64_t i) {
+    const std::uint64_t off = i * chunk;
+    const std::uint64_t len = std::min(chunk, bytes - off);
+    GPCX_CUDA(cudaMemcpyAsync(s.stage[i & 1].ptr, in + off, len, cudaMemcpyDeviceToHost,
+                              s.stream));
+    GPCX_CUDA(cudaEventRecord(s.chunk_done[i & 1], s.stream));
+  };
+  issue(0);
+  for (std::uint64_t i = 0; i < nchunks; ++i) {
+    if (i + 1 < nchunks) issue(i + 1);
+    GPCX_CUDA(cudaEventSynchronize(s.chunk_done[i & 1]));
+    const std::uint64_t off = i * chunk;
+    std::memcpy(out + off, s.stage[i & 1].ptr, std::min(chunk, bytes - off));
+  }
+}
+
+}  // namespace gpcx::rt

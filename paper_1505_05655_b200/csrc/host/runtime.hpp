@@ -1,0 +1,141 @@
+// runtime.hpp -- device context of the B200 backend: bound devices, per-device
+// pools of request slots (stream + device buffers + pinned staging), and the
+// host<->HBM staging helpers.
+//
+// This replaces the reference's payload staging, where every request lands
+// in a zero-filled pageable std::vector (proj/src/server.cpp:95-101) and is
+// copied again by the codec (proj/src/demosaic.cpp:177-209) and the response
+// framing (proj/src/registry.cpp:129).  Here a request's bytes go host ->
+// HBM once, with async copies on the slot's own stream; pageable callers are
+// staged through double-buffered pinned chunks so the memcpy of chunk i
+// overlaps the DMA of chunk i-1.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "../../../include/gpcx.h"
+
+namespace gpcx::rt {
+
+// Grow-only device allocation.
+struct DeviceBuf {
+  void* ptr = nullptr;
+  std::uint64_t cap = 0;
+  void ensure(std::uint64_t bytes, bool zero = false);
+  void release();
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct PinnedBuf {
+  void* ptr = nullptr;
+  std::uint64_t cap = 0;
+  void ensure(std::uint64_t bytes);
+  void release();
+};
+
+inline constexpr std::uint64_t kStageChunk = 8ull << 20;
+
+// Everything one in-flight request needs on one device.
+struct Slot {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t chunk_done[2] = {nullptr, nullptr};
+  DeviceBuf a, b, c;     // operands / result
+  DeviceBuf lut_ws;      // LUT workspace (zeroed once, self-cleaning)
+  DeviceBuf mm_ws;       // tensor-core matmul workspace
+  DeviceBuf small;       // LUT (128 KiB) + stats + hist
+  PinnedBuf stage[2];    // pageable-caller staging chunks
+  PinnedBuf h_small;     // stats readback
+  std::uint16_t* d_lut() const { return small.as<std::uint16_t>(); }
+  gpcx_lut_stats* d_stats() const {
+    return reinterpret_cast<gpcx_lut_stats*>(small.as<unsigned char>() + 131072);
+  }
+  std::uint32_t* d_hist() const {
+    return reinterpret_cast<std::uint32_t*>(small.as<unsigned char>() + 131072 + 256);
+  }
+  gpcx_lut_stats* h_stats() const { return static_cast<gpcx_lut_stats*>(h_small.ptr); }
+  ~Slot();
+};
+
+class Runtime;
+
+// RAII lease of a slot; returns it to its device pool.
+class SlotLease {
+ public:
+  SlotLease(Runtime* rt, Slot* slot) : rt_(rt), slot_(slot) {}
+  SlotLease(SlotLease&& o) noexcept : rt_(o.rt_), slot_(o.slot_) { o.slot_ = nullptr; }
+  SlotLease(const SlotLease&) = delete;
+  ~SlotLease();
+  Slot* operator->() const { return slot_; }
+  Slot& operator*() const { return *slot_; }
+
+ private:
+  Runtime* rt_;
+  Slot* slot_;
+};
+
+class Runtime {
+ public:
+  static Runtime& get();
+  // devices empty -> all visible devices.  Rebinding to a different set
+  // drains the pools first.
+  void init(const std::vector<int>& devices);
+  void shutdown();
+  std::vector<int> devices();
+  int ndev();
+  int pick_device_index();  // round robin over bound devices (C5 replicas)
+  SlotLease acquire(int device_index);
+  void release(Slot* slot);
+
+ private:
+  struct Pool {
+    int device;
+    std::vector<std::unique_ptr<Slot>> all;
+    std::vector<Slot*> free;
+  };
+  void ensure_init_locked();
+  std::mutex mu_;
+  bool inited_ = false;
+  std::vector<Pool> pools_;
+  std::atomic<unsigned> rr_{0};
+};
+
+// Host -> device copy on the slot stream.  Pinned sources go straight to the
+// DMA engine; pageable sources are staged chunk-wise (returns once the last
+// chunk's memcpy is issued; the caller syncs the stream before reusing src).
+void h2d(Slot& s, void* dst, const void* src, std::uint64_t bytes);
+// Device -> host copy on the slot stream; synchronises before returning.
+void d2h(Slot& s, void* dst, const void* src, std::uint64_t bytes);
+bool is_pinned(const void* p);
+
+// Pool of page-locked host buffers (cudaMallocHost costs ~ms per GiB, so
+// request/response staging buffers are recycled by power-of-two size class).
+class PinnedLease {
+ public:
+  PinnedLease() = default;
+  PinnedLease(void* p, std::uint64_t cap) : ptr_(p), cap_(cap) {}
+  PinnedLease(PinnedLease&& o) noexcept : ptr_(o.ptr_), cap_(o.cap_) { o.ptr_ = nullptr; }
+  PinnedLease& operator=(PinnedLease&& o) noexcept;
+  PinnedLease(const PinnedLease&) = delete;
+  ~PinnedLease();
+  void* get() const { return ptr_; }
+  std::uint64_t capacity() const { return cap_; }
+
+ private:
+  void* ptr_ = nullptr;
+  std::uint64_t cap_ = 0;
+};
+PinnedLease pinned_acquire(std::uint64_t bytes);
+void pinned_trim();  // frees idle pooled buffers
+
+// Makes `device` current for the calling thread.
+void use_device(int device);
+
+}  // namespace gpcx::rt

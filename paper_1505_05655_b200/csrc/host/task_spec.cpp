@@ -1,0 +1,110 @@
+// task_spec.cpp -- see task_spec.hpp.
+#include "task_spec.hpp"
+
+namespace gpcx::task {
+
+Flag flag_of(std::string_view flag) {
+  if (flag == "LUT_GEN") return Flag::LutGen;
+  if (flag == "LUT_APPLY") return Flag::LutApply;
+  if (flag == "LUT_CORRECT") return Flag::LutCorrect;
+  if (flag == "MATMUL") return Flag::Matmul;
+  fail(Errc::UnknownTask, std::string(flag));
+}
+
+const char* flag_name(Flag f) {
+  switch (f) {
+    case Flag::LutGen: return "LUT_GEN";
+    case Flag::LutApply: return "LUT_APPLY";
+    case Flag::LutCorrect: return "LUT_CORRECT";
+    case Flag::Matmul: return "MATMUL";
+  }
+  return "?";
+}
+
+std::vector<Flag> all_flags() {
+  return {Flag::LutApply, Flag::LutCorrect, Flag::LutGen, Flag::Matmul};
+}
+
+std::vector<std::string> required_params(Flag f) {
+  if (f == Flag::Matmul) return {"m", "k", "n"};
+  return {"rows", "cols"};
+}
+
+const char* mode_name(int mode) { return mode == GPCX_LUT_STRETCH ? "stretch" : "equalize"; }
+
+const char* prec_name(int prec) {
+  switch (prec) {
+    case GPCX_PREC_TF32: return "tf32";
+    case GPCX_PREC_BF16: return "bf16";
+    default: return "f32";
+  }
+}
+
+LutParams parse_lut(Flag f, const wire::ParamMap& params) {
+  LutParams p;
+  p.rows = params.get_uint("rows");
+  p.cols = params.get_uint("cols");
+  wire::dim_product("rows", p.rows, "cols", p.cols, 2);  // validates + caps
+  const std::string dtype = params.get_or("dtype", "u16");
+  if (dtype != "u16") fail(Errc::BadValue, "dtype=" + dtype);
+  if (f != Flag::LutApply) {
+    const std::string mode = params.get_or("mode", "equalize");
+    if (mode == "equalize") p.mode = GPCX_LUT_EQUALIZE;
+    else if (mode == "stretch") p.mode = GPCX_LUT_STRETCH;
+    else fail(Errc::BadValue, "mode=" + mode);
+  }
+  return p;
+}
+
+MatmulParams parse_matmul(const wire::ParamMap& params) {
+  MatmulParams p;
+  p.m = params.get_uint("m");
+  p.k = params.get_uint("k");
+  p.n = params.get_uint("n");
+  wire::capped_sum(wire::dim_product("m", p.m, "k", p.k, 4),
+                   wire::dim_product("k", p.k, "n", p.n, 4));
+  wire::dim_product("m", p.m, "n", p.n, 4);  // the response must fit too
+  const std::string prec = params.get_or("prec", "f32");
+  if (prec == "f32") p.prec = GPCX_PREC_F32;
+  else if (prec == "tf32") p.prec = GPCX_PREC_TF32;
+  else if (prec == "bf16") p.prec = GPCX_PREC_BF16;
+  else fail(Errc::BadValue, "prec=" + prec);
+  return p;
+}
+
+std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
+  switch (f) {
+    case Flag::LutGen:
+    case Flag::LutCorrect: {
+      const LutParams p = parse_lut(f, params);
+      return p.pixels() * 2;
+    }
+    case Flag::LutApply: {
+      const LutParams p = parse_lut(f, params);
+      return wire::capped_sum(kLutBytes, p.pixels() * 2);
+    }
+    case Flag::Matmul: {
+      const MatmulParams p = parse_matmul(params);
+      return (p.m * p.k + p.k * p.n) * 4;
+    }
+  }
+  return 0;
+}
+
+std::uint64_t output_len(Flag f, const wire::ParamMap& params) {
+  switch (f) {
+    case Flag::LutGen:
+      parse_lut(f, params);
+      return kLutBytes;
+    case Flag::LutApply:
+    case Flag::LutCorrect:
+      return parse_lut(f, params).pixels() * 2;
+    case Flag::Matmul: {
+      const MatmulParams p = parse_matmul(params);
+      return p.m * p.n * 4;
+    }
+  }
+  return 0;
+}
+
+}  // namespace gpcx::task

@@ -1,0 +1,58 @@
+// task_spec.hpp -- the GPU task flags: required params, payload / output
+// sizing and parameter parsing.  These are the TaskDescriptor pieces the
+// reference's built-in tasks define in proj/src/tasks.cpp:64-123 (sized_by ->
+// expected_payload_len, proj/src/wire.cpp:205-227), written for the flags of
+// SURVEY.md §8a':
+//
+//   flag         required       payload in                 payload out
+//   LUT_GEN      rows, cols     rows*cols u16 LE           65536 u16 LE (LUT)
+//   LUT_APPLY    rows, cols     LUT (131072 B) || image    rows*cols u16 LE
+//   LUT_CORRECT  rows, cols     rows*cols u16 LE           rows*cols u16 LE
+//   MATMUL       m, k, n        A (m*k f32) || B (k*n f32) C (m*n f32)
+//
+// Optional: dtype=u16 and mode=equalize|stretch (LUT_GEN / LUT_CORRECT) for
+// the LUT tasks, prec=f32|tf32|bf16 for MATMUL.  Sizes follow the
+// reference's dim_product() rules and the 1 GiB kMaxPayload cap.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "../../../include/gpcx.h"
+#include "wire.hpp"
+
+namespace gpcx::task {
+
+enum class Flag { LutGen, LutApply, LutCorrect, Matmul };
+
+inline constexpr std::uint64_t kLutBytes = 65536 * 2;
+
+Flag flag_of(std::string_view flag);  // UnknownTask
+const char* flag_name(Flag f);
+std::vector<Flag> all_flags();
+std::vector<std::string> required_params(Flag f);
+
+struct LutParams {
+  std::uint64_t rows = 0, cols = 0;
+  int mode = GPCX_LUT_EQUALIZE;
+  std::uint64_t pixels() const { return rows * cols; }
+};
+struct MatmulParams {
+  std::uint64_t m = 0, k = 0, n = 0;
+  int prec = GPCX_PREC_F32;
+};
+
+// Parse + validate (MissingParam / BadValue / Overflow).  Image byte count
+// is rows*cols*2 under the cap.
+LutParams parse_lut(Flag f, const wire::ParamMap& params);
+MatmulParams parse_matmul(const wire::ParamMap& params);
+
+std::uint64_t payload_len(Flag f, const wire::ParamMap& params);
+std::uint64_t output_len(Flag f, const wire::ParamMap& params);
+
+const char* mode_name(int mode);
+const char* prec_name(int prec);
+
+}  // namespace gpcx::task

@@ -1,0 +1,75 @@
+// kernels.hpp -- host-side launchers of the sm_100a kernels.
+//
+// All launchers are asynchronous on the given stream and throw
+// gpcx::Error(TaskFailed) on a launch failure.  Shapes are validated by the
+// callers (capi.cpp); launchers assume valid arguments.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/gpcx.h"
+
+namespace gpcx {
+
+namespace lut {
+
+inline constexpr int kBins = 65536;
+inline constexpr int kWords = kBins / 2;      // u16 pairs per u32 word
+inline constexpr int kMaxParts = 296;         // per-CTA partial histograms
+
+// Workspace layout (bytes):
+//   [0, 256 Ki)               overflow counters, u32[65536] (self-cleaning)
+//   [256 Ki, 512 Ki)          merged histogram, u32[65536]
+//   [512 Ki, +kMaxParts*8)    per-CTA (lo, hi) pairs for the min/max path
+//   [.. , + kMaxParts*128 Ki) per-CTA packed partial histograms
+std::uint64_t workspace_bytes();
+// The merged-histogram scratch inside a workspace (u32[65536]).
+std::uint32_t* ws_hist(void* ws);
+
+int parts_for(std::uint64_t n, int num_sms);
+
+void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
+                 void* ws, cudaStream_t stream);
+void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
+                      gpcx_lut_stats* stats, cudaStream_t stream);
+void launch_minmax(const std::uint16_t* img, std::uint64_t n,
+                   gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+void launch_from_minmax(const gpcx_lut_stats* stats, std::uint16_t* lut,
+                        cudaStream_t stream);
+void launch_apply(const std::uint16_t* lut, const std::uint16_t* in,
+                  std::uint16_t* out, std::uint64_t n, cudaStream_t stream);
+
+}  // namespace lut
+
+namespace synth {
+void launch_image(int kind, std::uint64_t seed, std::uint64_t rows,
+                  std::uint64_t cols, std::uint64_t row0, std::uint64_t nrows,
+                  std::uint16_t* out, cudaStream_t stream);
+void launch_matrix(int kind, std::uint64_t seed, std::uint64_t rows,
+                   std::uint64_t cols, std::uint64_t row0, std::uint64_t nrows,
+                   float* out, cudaStream_t stream);
+void launch_digest(const std::uint16_t* v, std::uint64_t n,
+                   std::uint64_t index0, std::uint64_t* digest,
+                   cudaStream_t stream);
+}  // namespace synth
+
+namespace gemm {
+// SIMT FP32 (reference precision).
+void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
+                  const float* A, std::uint64_t lda, const float* B,
+                  std::uint64_t ldb, float* C, std::uint64_t ldc,
+                  cudaStream_t stream);
+// Tensor-core path (tcgen05): prec = GPCX_PREC_TF32 / GPCX_PREC_BF16.
+std::uint64_t tc_workspace_bytes(int prec, std::uint64_t m, std::uint64_t n,
+                                 std::uint64_t k);
+void launch_tc(int prec, std::uint64_t m, std::uint64_t n, std::uint64_t k,
+               const float* A, std::uint64_t lda, const float* B,
+               std::uint64_t ldb, float* C, std::uint64_t ldc, void* ws,
+               cudaStream_t stream);
+}  // namespace gemm
+
+int device_sm_count();  // SMs of the current device (cached per device)
+
+}  // namespace gpcx

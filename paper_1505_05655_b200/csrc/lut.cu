@@ -1,0 +1,547 @@
+// lut.cu -- LUT generation and LUT-apply image correction for sm_100a.
+//
+// Task contract: SURVEY.md §8a' (LUT_GEN / LUT_APPLY / LUT_CORRECT), u16 LE
+// row-major samples as in the reference codec (proj/src/demosaic.cpp:177-209),
+// integer round-half-up as in proj/src/demosaic.cpp:37-46.  Results are
+// bit-identical to oracle/gpcx_oracle.c and independent of the CTA count /
+// GPU count (the parexec invariance contract, proj/include/gpc/parexec.hpp:11-31).
+//
+// Kernels (all HBM-bound; see DESIGN.md for the roofline of each):
+//   hist_kernel     persistent, 1 CTA/SM, 128 KiB smem histogram of packed
+//                   u16 pairs, 128-bit streaming loads.   2 B/px read.
+//   merge_kernel    column-sum of the per-CTA partials (+ overflow fixups).
+//   from_hist       1 CTA: block scan -> equalize LUT.
+//   minmax_kernel   warp-shuffle (redux) min/max for stretch.  2 B/px read.
+//   from_minmax     stretch LUT.
+//   apply_kernel    persistent, LUT staged in 128 KiB smem, 128-bit
+//                   loads/stores, 8 gathers per vector.   4 B/px.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "cuda_util.hpp"
+#include "kernels.hpp"
+
+namespace gpcx {
+
+int device_sm_count() {
+  static thread_local int cached_dev = -1;
+  static thread_local int cached_sms = 0;
+  int dev = 0;
+  GPCX_CUDA(cudaGetDevice(&dev));
+  if (dev != cached_dev) {
+    GPCX_CUDA(cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount,
+                                     dev));
+    cached_dev = dev;
+  }
+  return cached_sms;
+}
+
+namespace lut {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr std::uint64_t kOverflowOff = 0;
+constexpr std::uint64_t kHistOff = 256 * 1024;
+constexpr std::uint64_t kMinMaxOff = 512 * 1024;
+constexpr std::uint64_t kPartsOff = kMinMaxOff + 8 * 1024;
+constexpr int kSmemHist = kWords * 4;  // 128 KiB
+constexpr int kSmemLut = kBins * 2;    // 128 KiB
+constexpr int kUnroll = 4;
+
+static_assert(kMaxParts * 8 <= 8 * 1024, "min/max slot area");
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Count one sample into the packed smem histogram.  Word w holds bin 2w in
+// its low half and bin 2w+1 in its high half, so the word equals
+// count(2w) + 65536*count(2w+1) mod 2^32.  The thread whose atomic wraps a
+// half sees it in the returned old value and books the lost 65536 (and, for
+// a low-half carry into the high half, the spurious +1) into the global
+// overflow counters; the merge adds them back mod 2^32.  Exact for any
+// count < 2^32 and independent of the interleaving.
+__device__ __forceinline__ void count_one(std::uint32_t* bins,
+                                          std::uint32_t* overflow,
+                                          std::uint32_t v) {
+  const std::uint32_t hi_bin = v & 1u;
+  const std::uint32_t inc = hi_bin ? 0x10000u : 1u;
+  const std::uint32_t mask = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+  const std::uint32_t old = atomicAdd(&bins[v >> 1], inc);
+  if ((old & mask) == mask) {
+    atomicAdd(&overflow[v], 65536u);
+    if (!hi_bin) {
+      // carry into the high half: +1 there that is not a sample of v+1,
+      // and possibly a wrap of the high half itself.
+      atomicAdd(&overflow[v + 1],
+                (old >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
+    }
+  }
+}
+
+__device__ __forceinline__ void count_vec(std::uint32_t* bins,
+                                          std::uint32_t* overflow, uint4 q) {
+  count_one(bins, overflow, q.x & 0xFFFFu);
+  count_one(bins, overflow, q.x >> 16);
+  count_one(bins, overflow, q.y & 0xFFFFu);
+  count_one(bins, overflow, q.y >> 16);
+  count_one(bins, overflow, q.z & 0xFFFFu);
+  count_one(bins, overflow, q.z >> 16);
+  count_one(bins, overflow, q.w & 0xFFFFu);
+  count_one(bins, overflow, q.w >> 16);
+}
+
+// Samples before the first 16-byte boundary (pointers are at least 2-byte
+// aligned), rounded to whole samples.
+__device__ __host__ __forceinline__ std::uint64_t head_len(const void* p,
+                                                           std::uint64_t n) {
+  const std::uint64_t mis = reinterpret_cast<std::uintptr_t>(p) & 15u;
+  const std::uint64_t h = ((16u - mis) & 15u) >> 1;
+  return h < n ? h : n;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    hist_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
+                std::uint32_t* __restrict__ parts,
+                std::uint32_t* __restrict__ overflow) {
+  extern __shared__ uint4 smem_u4[];
+  std::uint32_t* bins = reinterpret_cast<std::uint32_t*>(smem_u4);
+  for (int i = threadIdx.x; i < kWords / 4; i += kThreads)
+    smem_u4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  const std::uint64_t head = head_len(img, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  if (blockIdx.x == 0) {
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads)
+      count_one(bins, overflow, img[i]);
+  }
+  if (blockIdx.x == gridDim.x - 1) {
+    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
+      count_one(bins, overflow, img[i]);
+  }
+
+  const uint4* body = reinterpret_cast<const uint4*>(img + head);
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
+  std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+    uint4 q[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(body + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) count_vec(bins, overflow, q[u]);
+  }
+  for (; i < nvec; i += stride) count_vec(bins, overflow, ld_stream(body + i));
+  __syncthreads();
+
+  uint4* dst = reinterpret_cast<uint4*>(parts + static_cast<std::uint64_t>(blockIdx.x) * kWords);
+  for (int j = threadIdx.x; j < kWords / 4; j += kThreads) dst[j] = smem_u4[j];
+}
+
+// hist[2w], hist[2w+1] = column sums of the packed partials + overflow;
+// leaves the overflow counters zeroed for the next call.
+__global__ void __launch_bounds__(256)
+    merge_kernel(const std::uint32_t* __restrict__ parts, int nparts,
+                 std::uint32_t* __restrict__ overflow,
+                 std::uint32_t* __restrict__ hist) {
+  const int w = blockIdx.x * 256 + threadIdx.x;
+  if (w >= kWords) return;
+  std::uint32_t lo = 0, hi = 0;
+  int p = 0;
+  for (; p + 4 <= nparts; p += 4) {
+    std::uint32_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = parts[static_cast<std::uint64_t>(p + u) * kWords + w];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      lo += x[u] & 0xFFFFu;
+      hi += x[u] >> 16;
+    }
+  }
+  for (; p < nparts; ++p) {
+    const std::uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
+    lo += x & 0xFFFFu;
+    hi += x >> 16;
+  }
+  const uint2 ov = reinterpret_cast<const uint2*>(overflow)[w];
+  reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
+  reinterpret_cast<uint2*>(hist)[w] = make_uint2(lo + ov.x, hi + ov.y);
+}
+
+// Block-wide exclusive scan of one u32 per thread (1024 threads).
+__device__ __forceinline__ std::uint32_t block_exclusive_scan(std::uint32_t x,
+                                                              std::uint32_t* sh,
+                                                              std::uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  std::uint32_t inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) sh[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    std::uint32_t s = sh[lane];
+    std::uint32_t sinc = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, sinc, d);
+      if (lane >= d) sinc += y;
+    }
+    sh[lane] = sinc - s;  // exclusive warp offsets
+    if (lane == 31) sh[32] = sinc;
+  }
+  __syncthreads();
+  *total = sh[32];
+  return sh[warp] + inc - x;
+}
+
+// LUT entry for bin v given the statistics (SURVEY §8a' formulas).
+__device__ __forceinline__ std::uint32_t equalize_entry(std::uint32_t v,
+                                                        std::uint64_t cdf,
+                                                        std::uint64_t cdf_min,
+                                                        std::uint64_t d,
+                                                        std::uint32_t lo) {
+  if (d == 0) return v;
+  if (v < lo) return 0;
+  return static_cast<std::uint32_t>(((cdf - cdf_min) * 65535u + d / 2) / d);
+}
+
+__device__ __forceinline__ std::uint32_t stretch_entry(std::uint64_t v,
+                                                       std::uint64_t n,
+                                                       std::uint64_t lo,
+                                                       std::uint64_t hi) {
+  const std::uint64_t span = hi - lo;
+  if (n == 0 || span == 0) return static_cast<std::uint32_t>(v);
+  if (v <= lo) return 0;
+  if (v >= hi) return 65535;
+  return static_cast<std::uint32_t>(((v - lo) * 65535u + span / 2) / span);
+}
+
+// Equalize (or stretch, from the histogram's extremes) LUT.  One CTA of
+// 1024 threads, 64 consecutive bins per thread: pass 1 sums the thread's
+// bins (block scan -> cdf offsets, redux min/max -> lo/hi), pass 2 re-reads
+// them from L2 and writes 8 LUT entries per 128-bit store.
+__global__ void __launch_bounds__(1024, 1)
+    from_hist_kernel(const std::uint32_t* __restrict__ hist, int mode,
+                     std::uint16_t* __restrict__ lut,
+                     gpcx_lut_stats* __restrict__ stats) {
+  __shared__ std::uint32_t sh[33];
+  __shared__ std::uint32_t s_lo, s_hi;
+  const int t = threadIdx.x;
+  const int b0 = t * 64;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + b0);
+  std::uint32_t sum = 0;
+  std::uint32_t first = 0xFFFFFFFFu, last = 0;
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    const uint4 q = h4[j];
+    const std::uint32_t e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      sum += e[u];
+      if (e[u] != 0) {
+        if (first == 0xFFFFFFFFu) first = b0 + 4 * j + u;
+        last = b0 + 4 * j + u;
+      }
+    }
+  }
+  if (t == 0) {
+    s_lo = 0xFFFFFFFFu;
+    s_hi = 0;
+  }
+  std::uint32_t n32;
+  const std::uint32_t excl = block_exclusive_scan(sum, sh, &n32);
+  // block_exclusive_scan's barriers order t==0's init before the atomics.
+  const std::uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, first);
+  const std::uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, sum != 0 ? last : 0);
+  if ((t & 31) == 0) {
+    atomicMin(&s_lo, wmin);
+    atomicMax(&s_hi, wmax);
+  }
+  __syncthreads();
+  const std::uint32_t lo = s_lo, hi = s_hi;
+  const std::uint64_t n = n32;
+  uint4* dst = reinterpret_cast<uint4*>(lut + b0);
+  if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
+    for (int j = 0; j < 8; ++j) {
+      const std::uint32_t v = b0 + 8 * j;
+      dst[j] = make_uint4(v | ((v + 1) << 16), (v + 2) | ((v + 3) << 16),
+                          (v + 4) | ((v + 5) << 16), (v + 6) | ((v + 7) << 16));
+    }
+    if (t == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
+    return;
+  }
+  const std::uint64_t cdf_min = hist[lo];
+  if (t == 0) *stats = gpcx_lut_stats{n, lo, hi, cdf_min};
+  const std::uint64_t d = n - cdf_min;
+  std::uint64_t cdf = excl;
+  for (int j = 0; j < 8; ++j) {
+    std::uint32_t w[4];
+    const uint4 qa = h4[2 * j], qb = h4[2 * j + 1];
+    const std::uint32_t e[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const std::uint32_t v = b0 + 8 * j + u;
+      cdf += e[u];
+      const std::uint32_t r = (mode == GPCX_LUT_STRETCH)
+                                  ? stretch_entry(v, n, lo, hi)
+                                  : equalize_entry(v, cdf, cdf_min, d, lo);
+      if (u & 1) w[u >> 1] |= r << 16;
+      else w[u >> 1] = r;
+    }
+    dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ void minmax_vec(uint4 q, std::uint32_t& mn2,
+                                           std::uint32_t& mx2) {
+  mn2 = __vminu2(mn2, __vminu2(__vminu2(q.x, q.y), __vminu2(q.z, q.w)));
+  mx2 = __vmaxu2(mx2, __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w)));
+}
+
+// Per-CTA (lo, hi) of the samples; SIMD u16x2 min/max per thread, then
+// redux.sync warp reductions and a 32-entry smem step.
+__global__ void __launch_bounds__(kThreads)
+    minmax_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
+                  uint2* __restrict__ slots) {
+  __shared__ std::uint32_t smn[32], smx[32];
+  std::uint32_t mn2 = 0xFFFFFFFFu, mx2 = 0;
+  const std::uint64_t head = head_len(img, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
+  if (tid < head) {
+    const std::uint32_t v = img[tid];
+    mn2 = __vminu2(mn2, v | (v << 16));
+    mx2 = __vmaxu2(mx2, v | (v << 16));
+  }
+  if (tid < n - tail0) {
+    const std::uint32_t v = img[tail0 + tid];
+    mn2 = __vminu2(mn2, v | (v << 16));
+    mx2 = __vmaxu2(mx2, v | (v << 16));
+  }
+  const uint4* body = reinterpret_cast<const uint4*>(img + head);
+  std::uint64_t i = tid;
+  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+    uint4 q[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(body + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) minmax_vec(q[u], mn2, mx2);
+  }
+  for (; i < nvec; i += stride) minmax_vec(ld_stream(body + i), mn2, mx2);
+
+  std::uint32_t mn = min(mn2 & 0xFFFFu, mn2 >> 16);
+  std::uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
+  mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    smn[warp] = mn;
+    smx[warp] = mx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    mn = __reduce_min_sync(0xFFFFFFFFu, smn[lane]);
+    mx = __reduce_max_sync(0xFFFFFFFFu, smx[lane]);
+    if (lane == 0) slots[blockIdx.x] = make_uint2(mn, mx);
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    minmax_reduce_kernel(const uint2* __restrict__ slots, int nslots,
+                         std::uint64_t n, gpcx_lut_stats* __restrict__ stats) {
+  __shared__ std::uint32_t smn[32], smx[32];
+  std::uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  for (int i = threadIdx.x; i < nslots; i += 1024) {
+    const uint2 s = slots[i];
+    mn = min(mn, s.x);
+    mx = max(mx, s.y);
+  }
+  mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    smn[warp] = mn;
+    smx[warp] = mx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    mn = __reduce_min_sync(0xFFFFFFFFu, smn[lane]);
+    mx = __reduce_max_sync(0xFFFFFFFFu, smx[lane]);
+    if (lane == 0) {
+      if (n == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
+      else *stats = gpcx_lut_stats{n, mn, mx, 0};
+    }
+  }
+}
+
+// Stretch LUT from (lo, hi): 64 entries per thread of one 1024-thread CTA.
+__global__ void __launch_bounds__(1024)
+    from_minmax_kernel(const gpcx_lut_stats* __restrict__ stats,
+                       std::uint16_t* __restrict__ lut) {
+  const std::uint64_t n = stats->n;
+  const std::uint64_t lo = stats->lo, hi = stats->hi;
+  const int b0 = threadIdx.x * 64;
+  uint4* dst = reinterpret_cast<uint4*>(lut + b0);
+  for (int j = 0; j < 8; ++j) {
+    std::uint32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const std::uint32_t r = stretch_entry(b0 + 8 * j + u, n, lo, hi);
+      if (u & 1) w[u >> 1] |= r << 16;
+      else w[u >> 1] = r;
+    }
+    dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
+  uint4 r;
+  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.x >> 16]) << 16);
+  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.y >> 16]) << 16);
+  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.z >> 16]) << 16);
+  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.w >> 16]) << 16);
+  return r;
+}
+
+// out = LUT[in].  The 128 KiB LUT is staged once per CTA in shared memory
+// (1 CTA/SM, persistent grid); the image streams through with 128-bit
+// loads/stores, kUnroll vectors in flight per thread.
+__global__ void __launch_bounds__(kThreads, 1)
+    apply_kernel(const std::uint16_t* __restrict__ lut_g,
+                 const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
+                 int vector_ok) {
+  extern __shared__ uint4 smem_u4[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(lut_g);
+    for (int i = threadIdx.x; i < kBins / 8; i += kThreads) smem_u4[i] = src[i];
+  }
+  __syncthreads();
+  const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
+  const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
+
+  if (!vector_ok) {  // mismatched alignment of in/out: scalar path
+    for (std::uint64_t i = tid; i < n; i += stride) out[i] = s_lut[in[i]];
+    return;
+  }
+  const std::uint64_t head = head_len(in, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  if (tid < head) out[tid] = s_lut[in[tid]];
+  if (tid < n - tail0) out[tail0 + tid] = s_lut[in[tail0 + tid]];
+
+  const uint4* src = reinterpret_cast<const uint4*>(in + head);
+  uint4* dst = reinterpret_cast<uint4*>(out + head);
+  std::uint64_t i = tid;
+  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+    uint4 q[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
+  }
+  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
+}
+
+bool g_attrs_set[64] = {};
+
+void set_attrs_once() {
+  int dev = 0;
+  GPCX_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && g_attrs_set[dev]) return;
+  GPCX_CUDA(cudaFuncSetAttribute(hist_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemHist));
+  GPCX_CUDA(cudaFuncSetAttribute(apply_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLut));
+  if (dev < 64) g_attrs_set[dev] = true;
+}
+
+}  // namespace
+
+std::uint32_t* ws_hist(void* ws) {
+  return reinterpret_cast<std::uint32_t*>(static_cast<unsigned char*>(ws) + kHistOff);
+}
+
+std::uint64_t workspace_bytes() {
+  return kPartsOff + static_cast<std::uint64_t>(kMaxParts) * kWords * 4;
+}
+
+int parts_for(std::uint64_t n, int num_sms) {
+  // One CTA per SM once there is enough work; at least 64 Ki samples per
+  // CTA below that so the per-CTA partial flush stays amortised.
+  const std::uint64_t want = (n + 65535) / 65536;
+  int p = static_cast<int>(std::min<std::uint64_t>(want, static_cast<std::uint64_t>(num_sms)));
+  return std::max(1, std::min(p, kMaxParts));
+}
+
+void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
+                 void* ws, cudaStream_t stream) {
+  set_attrs_once();
+  auto* base = static_cast<unsigned char*>(ws);
+  auto* overflow = reinterpret_cast<std::uint32_t*>(base + kOverflowOff);
+  auto* parts = reinterpret_cast<std::uint32_t*>(base + kPartsOff);
+  const int p = parts_for(n, device_sm_count());
+  hist_kernel<<<p, kThreads, kSmemHist, stream>>>(img, n, parts, overflow);
+  GPCX_LAUNCH_CHECK();
+  merge_kernel<<<kWords / 256, 256, 0, stream>>>(parts, p, overflow, hist);
+  GPCX_LAUNCH_CHECK();
+}
+
+void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
+                      gpcx_lut_stats* stats, cudaStream_t stream) {
+  from_hist_kernel<<<1, 1024, 0, stream>>>(hist, mode, lut, stats);
+  GPCX_LAUNCH_CHECK();
+}
+
+void launch_minmax(const std::uint16_t* img, std::uint64_t n,
+                   gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  auto* slots = reinterpret_cast<uint2*>(static_cast<unsigned char*>(ws) + kMinMaxOff);
+  const int p = std::min(kMaxParts, std::max(1, static_cast<int>(std::min<std::uint64_t>(
+                                                    (n + 65535) / 65536,
+                                                    static_cast<std::uint64_t>(2 * device_sm_count())))));
+  minmax_kernel<<<p, kThreads, 0, stream>>>(img, n, slots);
+  GPCX_LAUNCH_CHECK();
+  minmax_reduce_kernel<<<1, 1024, 0, stream>>>(slots, p, n, stats);
+  GPCX_LAUNCH_CHECK();
+}
+
+void launch_from_minmax(const gpcx_lut_stats* stats, std::uint16_t* lut,
+                        cudaStream_t stream) {
+  from_minmax_kernel<<<1, 1024, 0, stream>>>(stats, lut);
+  GPCX_LAUNCH_CHECK();
+}
+
+void launch_apply(const std::uint16_t* lut, const std::uint16_t* in,
+                  std::uint16_t* out, std::uint64_t n, cudaStream_t stream) {
+  if (n == 0) return;
+  set_attrs_once();
+  const int vector_ok =
+      ((reinterpret_cast<std::uintptr_t>(in) ^ reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
+  const std::uint64_t want = (n + 8191) / 8192;
+  const int p = static_cast<int>(std::max<std::uint64_t>(
+      1, std::min<std::uint64_t>(want, static_cast<std::uint64_t>(device_sm_count()))));
+  apply_kernel<<<p, kThreads, kSmemLut, stream>>>(lut, in, out, n, vector_ok);
+  GPCX_LAUNCH_CHECK();
+}
+
+}  // namespace lut
+}  // namespace gpcx

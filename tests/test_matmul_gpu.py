@@ -1,0 +1,118 @@
+"""MATMUL on the B200 vs the f64 CPU oracle.
+
+Tolerances (stated here as the contract):
+  |c - c_ref| <= tol * sum_k |a_ik||b_kj|
+  f32  (SIMT, fp32 accumulate)               tol = 1e-5
+  tf32 (tcgen05 kind::tf32, RNA-rounded in)  tol = 1e-5 vs the oracle run on
+        the same tf32-rounded operands (2e-3 vs the unrounded f32 operands)
+  bf16 (tcgen05 kind::f16, RNE-rounded in)   tol = 1e-5 vs the oracle run on
+        the same bf16-rounded operands (1.6e-2 vs the unrounded operands)
+exact8 operands (k * 2^-7) make every product exact: any accumulation order
+gives the same bits while sums stay below 2^24 ulps, so small-k exact8
+cases are compared bit-for-bit.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1505_05655_b200 as G
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {O.PREC_F32: 1e-5, O.PREC_TF32: 1e-5, O.PREC_BF16: 1e-5}
+TOL_UNROUNDED = {O.PREC_F32: 1e-5, O.PREC_TF32: 2e-3, O.PREC_BF16: 1.6e-2}
+PREC_NAME = {O.PREC_F32: "f32", O.PREC_TF32: "tf32", O.PREC_BF16: "bf16"}
+
+
+def _mats(kind, seed, m, k, n):
+    A = O.synth_matrix(kind, seed, m, k)
+    B = O.synth_matrix(kind, O.seed_b(seed), k, n)
+    return A, B
+
+
+def _check(Cg, A, B, prec, rows=None):
+    Ar = O.round_matrix(prec, A) if prec != O.PREC_F32 else A
+    Br = O.round_matrix(prec, B) if prec != O.PREC_F32 else B
+    Cref, ab = O.matmul_f64(Ar, Br, rows)
+    got = Cg if rows is None else Cg[rows]
+    err = np.abs(got.astype(np.float64) - Cref)
+    bound = TOL[prec] * ab + 1e-30
+    worst = float(np.max(err / bound)) if err.size else 0.0
+    assert np.all(err <= bound), f"prec={PREC_NAME[prec]} worst err/bound={worst:.3g}"
+    C0, ab0 = O.matmul_f64(A, B, rows)
+    assert np.all(np.abs(got.astype(np.float64) - C0) <= TOL_UNROUNDED[prec] * ab0 + 1e-30)
+
+
+def _run_device(prec, A, B):
+    import torch
+    from paper_1505_05655_b200 import device as D
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    dC = torch.full((A.shape[0], B.shape[1]), float("nan"), device="cuda")
+    ws = D.matmul_workspace(prec, A.shape[0], B.shape[1], A.shape[1])
+    D.matmul(prec, dA, dB, dC, ws)
+    return dC.cpu().numpy()
+
+
+SHAPES = [(128, 128, 16), (256, 384, 512), (1, 1, 1), (3, 5, 7), (129, 130, 131), (1000, 17, 300),
+          (64, 1024, 4096)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("kind", [O.MAT_UNIFORM32, O.MAT_EXACT8])
+def test_sgemm_within_tolerance(gpu, m, n, k, kind):
+    A, B = _mats(kind, 0x5EED, m, k, n)
+    _check(_run_device(O.PREC_F32, A, B), A, B, O.PREC_F32)
+
+
+def test_sgemm_exact8_bit_exact(gpu):
+    A, B = _mats(O.MAT_EXACT8, 9, 256, 512, 384)
+    Cg = _run_device(O.PREC_F32, A, B)
+    Cref, _ = O.matmul_f64(A, B)
+    assert np.array_equal(Cg.astype(np.float64), Cref)
+
+
+def test_sgemm_strided_operands(gpu):
+    import torch
+    from paper_1505_05655_b200 import device as D
+    A, B = _mats(O.MAT_UNIFORM32, 3, 200, 96, 160)
+    big_a = torch.zeros(200, 100, device="cuda")
+    big_a[:, :96] = torch.from_numpy(A)
+    big_b = torch.zeros(96, 170, device="cuda")
+    big_b[:, :160] = torch.from_numpy(B)
+    big_c = torch.zeros(200, 165, device="cuda")
+    D.matmul(O.PREC_F32, big_a[:, :96], big_b[:, :160], big_c[:, :160])
+    _check(big_c[:, :160].cpu().numpy(), A, B, O.PREC_F32)
+    assert float(big_c[:, 160:].abs().max()) == 0.0
+
+
+def test_sgemm_c2_size_sampled(gpu):
+    """Config C2 (4096^3, f32) checked on 64 sampled rows."""
+    A, B = _mats(O.MAT_UNIFORM32, 0x5EED, 4096, 4096, 4096)
+    Cg = _run_device(O.PREC_F32, A, B)
+    rows = np.linspace(0, 4095, 64).astype(np.uint64)
+    _check(Cg, A, B, O.PREC_F32, rows)
+
+
+def test_gpcx_run_matmul_f32(gpu):
+    m, k, n = 70, 90, 110
+    A, B = _mats(O.MAT_UNIFORM32, 5, m, k, n)
+    res, payload = G.run("MATMUL", f"m={m},k={k},n={n}", np.concatenate([A.ravel(), B.ravel()]))
+    assert res == {"m": str(m), "n": str(n), "k": str(k), "prec": "f32"}
+    _check(payload.view(np.float32).reshape(m, n), A, B, O.PREC_F32)
+
+
+def test_gpcx_run_matmul_block_rows_invariant(gpu):
+    """Block-row sharding (device 0 bound 3x) gives the bitwise same C."""
+    m, k, n = 4096, 4096, 4096  # 1.4e11 flop: above the sharding threshold
+    A, B = _mats(O.MAT_UNIFORM32, 6, m, k, n)
+    payload_in = np.concatenate([A.ravel(), B.ravel()])
+    _, one = G.run("MATMUL", f"m={m},k={k},n={n}", payload_in)
+    try:
+        G.init([0, 0, 0])
+        _, three = G.run("MATMUL", f"m={m},k={k},n={n}", payload_in)
+    finally:
+        G.init([0])
+    assert np.array_equal(one, three)
