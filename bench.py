@@ -66,46 +66,60 @@ def peaks() -> dict:
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """NVML sampler (the data nvidia-smi's clocks line reports) polling every
+    2 ms during the timed region -- the LUT step is ~1 ms, far below
+    nvidia-smi's sampling period -- plus one sample at entry and exit."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReasons bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+    }
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows: list[list[str]] = []
-        self._proc = None
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nv = None
+
+    def _sample(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except AttributeError:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append((sm, rs))
+
+    def _loop(self):
+        while not self._stop.wait(0.002):
+            self._sample()
 
     def __enter__(self):
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._sample()
+            self._t = threading.Thread(target=self._loop, daemon=True)
             self._t.start()
-        except OSError:
-            self._proc = None
+        except Exception:  # no NVML: report no samples rather than guess
+            self._nv = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
-
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            self._proc.wait(timeout=5)
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join()
+            self._sample()
 
     def summary(self) -> dict:
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 9
-                          for i, v in enumerate(r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({name for _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, 2 ms polling"}
 
 
 # ------------------------------------------------------------------ dist ---

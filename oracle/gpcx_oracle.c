@@ -114,7 +114,7 @@ int orc_lut_from_hist(const uint64_t* hist, int mode, uint16_t* lut,
   stats->n = n;
   stats->lo = (uint32_t)lo;
   stats->hi = (uint32_t)hi;
-  stats->cdf_min = hist[lo];
+  stats->cdf_min = (mode == ORC_LUT_STRETCH) ? 0 : hist[lo]; /* equalize only */
 
   if (mode == ORC_LUT_STRETCH) {
     const uint64_t span = (uint64_t)(hi - lo);

@@ -182,44 +182,28 @@ __global__ void __launch_bounds__(256)
   reinterpret_cast<uint2*>(hist)[w] = make_uint2(lo + ov.x, hi + ov.y);
 }
 
-// Block-wide exclusive scan of one u32 per thread (1024 threads).
-__device__ __forceinline__ std::uint32_t block_exclusive_scan(std::uint32_t x,
-                                                              std::uint32_t* sh,
-                                                              std::uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  std::uint32_t inc = x;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += y;
-  }
-  if (lane == 31) sh[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    std::uint32_t s = sh[lane];
-    std::uint32_t sinc = s;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, sinc, d);
-      if (lane >= d) sinc += y;
-    }
-    sh[lane] = sinc - s;  // exclusive warp offsets
-    if (lane == 31) sh[32] = sinc;
-  }
-  __syncthreads();
-  *total = sh[32];
-  return sh[warp] + inc - x;
+// floor(num / d) for num < 2^50 and d >= 1 without a 64-bit integer divide
+// (a ~70-instruction software sequence): the f64 estimate num * (1/d) is
+// within 1/8 of the true quotient, so truncation is off by at most one and a
+// single remainder test fixes it.  Bit-exact with the oracle's integer '/'.
+__device__ __forceinline__ std::uint64_t udiv_exact(std::uint64_t num, std::uint64_t d,
+                                                    double inv_d) {
+  std::uint64_t q = static_cast<std::uint64_t>(static_cast<double>(num) * inv_d);
+  const auto r = static_cast<long long>(num - q * d);
+  if (r < 0) --q;
+  else if (static_cast<std::uint64_t>(r) >= d) ++q;
+  return q;
 }
 
 // LUT entry for bin v given the statistics (SURVEY §8a' formulas).
 __device__ __forceinline__ std::uint32_t equalize_entry(std::uint32_t v,
                                                         std::uint64_t cdf,
                                                         std::uint64_t cdf_min,
-                                                        std::uint64_t d,
+                                                        std::uint64_t d, double inv_d,
                                                         std::uint32_t lo) {
   if (d == 0) return v;
   if (v < lo) return 0;
-  return static_cast<std::uint32_t>(((cdf - cdf_min) * 65535u + d / 2) / d);
+  return static_cast<std::uint32_t>(udiv_exact((cdf - cdf_min) * 65535u + d / 2, d, inv_d));
 }
 
 __device__ __forceinline__ std::uint32_t stretch_entry(std::uint64_t v,
@@ -230,82 +214,94 @@ __device__ __forceinline__ std::uint32_t stretch_entry(std::uint64_t v,
   if (n == 0 || span == 0) return static_cast<std::uint32_t>(v);
   if (v <= lo) return 0;
   if (v >= hi) return 65535;
-  return static_cast<std::uint32_t>(((v - lo) * 65535u + span / 2) / span);
+  return static_cast<std::uint32_t>(
+      udiv_exact((v - lo) * 65535u + span / 2, span, 1.0 / static_cast<double>(span)));
 }
 
-// Equalize (or stretch, from the histogram's extremes) LUT.  One CTA of
-// 1024 threads, 64 consecutive bins per thread: pass 1 sums the thread's
-// bins (block scan -> cdf offsets, redux min/max -> lo/hi), pass 2 re-reads
-// them from L2 and writes 8 LUT entries per 128-bit store.
+// Equalize (or stretch, from the histogram's extremes) LUT.  One CTA of 32
+// warps; warp w owns bins [2048w, 2048w + 2048) and walks them 32 at a time
+// with coalesced 128-byte loads.  Pass 1: per-warp totals and first / last
+// non-empty bin; a 32-entry scan gives every warp its cdf offset.  Pass 2:
+// warp-shuffle inclusive scan of each 32-bin row -> cdf -> LUT entries,
+// written as coalesced 64-byte rows.
 __global__ void __launch_bounds__(1024, 1)
     from_hist_kernel(const std::uint32_t* __restrict__ hist, int mode,
                      std::uint16_t* __restrict__ lut,
                      gpcx_lut_stats* __restrict__ stats) {
-  __shared__ std::uint32_t sh[33];
-  __shared__ std::uint32_t s_lo, s_hi;
-  const int t = threadIdx.x;
-  const int b0 = t * 64;
-  const uint4* h4 = reinterpret_cast<const uint4*>(hist + b0);
-  std::uint32_t sum = 0;
-  std::uint32_t first = 0xFFFFFFFFu, last = 0;
-#pragma unroll 4
-  for (int j = 0; j < 16; ++j) {
-    const uint4 q = h4[j];
-    const std::uint32_t e[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      sum += e[u];
-      if (e[u] != 0) {
-        if (first == 0xFFFFFFFFu) first = b0 + 4 * j + u;
-        last = b0 + 4 * j + u;
-      }
+  constexpr int kRows = kBins / 1024;  // 64 rows of 32 bins per warp
+  __shared__ std::uint32_t s_tot[32], s_lo[32], s_hi[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint32_t base = static_cast<std::uint32_t>(warp) * (kRows * 32);
+  const std::uint32_t* hw = hist + base + lane;
+
+  std::uint32_t acc = 0, first = 0xFFFFFFFFu, last = 0;
+#pragma unroll 8
+  for (int r = 0; r < kRows; ++r) {
+    const std::uint32_t x = __ldg(hw + r * 32);
+    acc += x;
+    if (x != 0) {
+      first = min(first, base + r * 32 + lane);
+      last = base + r * 32 + lane;
     }
   }
-  if (t == 0) {
-    s_lo = 0xFFFFFFFFu;
-    s_hi = 0;
-  }
-  std::uint32_t n32;
-  const std::uint32_t excl = block_exclusive_scan(sum, sh, &n32);
-  // block_exclusive_scan's barriers order t==0's init before the atomics.
-  const std::uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, first);
-  const std::uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, sum != 0 ? last : 0);
-  if ((t & 31) == 0) {
-    atomicMin(&s_lo, wmin);
-    atomicMax(&s_hi, wmax);
+  const std::uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, acc);
+  const std::uint32_t wlo = __reduce_min_sync(0xFFFFFFFFu, first);
+  const std::uint32_t whi = __reduce_max_sync(0xFFFFFFFFu, last);
+  if (lane == 0) {
+    s_tot[warp] = wtot;
+    s_lo[warp] = wlo;
+    s_hi[warp] = wtot != 0 ? whi : 0;
   }
   __syncthreads();
-  const std::uint32_t lo = s_lo, hi = s_hi;
+  // every warp redoes the 32-entry reductions (cheaper than another barrier)
+  const std::uint32_t t = s_tot[lane];
+  std::uint32_t incl = t;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const std::uint32_t n32 = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  const std::uint32_t offset = __shfl_sync(0xFFFFFFFFu, incl - t, warp);
+  const std::uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, s_lo[lane]);
+  const std::uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, s_hi[lane]);
   const std::uint64_t n = n32;
-  uint4* dst = reinterpret_cast<uint4*>(lut + b0);
+
+  std::uint16_t* lw = lut + base + lane;
   if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
-    for (int j = 0; j < 8; ++j) {
-      const std::uint32_t v = b0 + 8 * j;
-      dst[j] = make_uint4(v | ((v + 1) << 16), (v + 2) | ((v + 3) << 16),
-                          (v + 4) | ((v + 5) << 16), (v + 6) | ((v + 7) << 16));
-    }
-    if (t == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
+    for (int r = 0; r < kRows; ++r) lw[r * 32] = static_cast<std::uint16_t>(base + r * 32 + lane);
+    if (threadIdx.x == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
     return;
   }
-  const std::uint64_t cdf_min = hist[lo];
-  if (t == 0) *stats = gpcx_lut_stats{n, lo, hi, cdf_min};
+  const std::uint64_t cdf_min = __ldg(hist + lo);
+  if (threadIdx.x == 0)
+    *stats = gpcx_lut_stats{n, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
   const std::uint64_t d = n - cdf_min;
-  std::uint64_t cdf = excl;
-  for (int j = 0; j < 8; ++j) {
-    std::uint32_t w[4];
-    const uint4 qa = h4[2 * j], qb = h4[2 * j + 1];
-    const std::uint32_t e[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+  const double inv_d = d != 0 ? 1.0 / static_cast<double>(d) : 0.0;
+  const std::uint64_t span = hi - lo;
+  const double inv_span = span != 0 ? 1.0 / static_cast<double>(span) : 0.0;
+  std::uint64_t carry = offset;
+#pragma unroll 4
+  for (int r = 0; r < kRows; ++r) {
+    const std::uint32_t v = base + r * 32 + lane;
+    std::uint32_t x = __ldg(hw + r * 32);
+    std::uint32_t inc = x;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const std::uint32_t v = b0 + 8 * j + u;
-      cdf += e[u];
-      const std::uint32_t r = (mode == GPCX_LUT_STRETCH)
-                                  ? stretch_entry(v, n, lo, hi)
-                                  : equalize_entry(v, cdf, cdf_min, d, lo);
-      if (u & 1) w[u >> 1] |= r << 16;
-      else w[u >> 1] = r;
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, dd);
+      if (lane >= dd) inc += y;
     }
-    dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+    std::uint32_t e;
+    if (mode == GPCX_LUT_STRETCH) {
+      if (span == 0) e = v;
+      else if (v <= lo) e = 0;
+      else if (v >= hi) e = 65535;
+      else e = static_cast<std::uint32_t>(udiv_exact((v - lo) * 65535ull + span / 2, span, inv_span));
+    } else {
+      e = equalize_entry(v, carry + inc, cdf_min, d, inv_d, lo);
+    }
+    lw[r * 32] = static_cast<std::uint16_t>(e);
+    carry += __shfl_sync(0xFFFFFFFFu, inc, 31);
   }
 }
 

@@ -51,7 +51,7 @@ def lut(img: np.ndarray, mode: str) -> tuple[np.ndarray, dict]:
         return v.astype(np.uint16), {"n": 0, "lo": 0, "hi": 0, "cdf_min": 0}
     lo, hi = int(nz[0]), int(nz[-1])
     n = int(hist.sum())
-    st = {"n": n, "lo": lo, "hi": hi, "cdf_min": int(hist[lo])}
+    st = {"n": n, "lo": lo, "hi": hi, "cdf_min": int(hist[lo]) if mode == "equalize" else 0}
     if mode == "stretch":
         if hi == lo:
             return v.astype(np.uint16), st

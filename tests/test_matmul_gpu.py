@@ -96,6 +96,56 @@ def test_sgemm_c2_size_sampled(gpu):
     _check(Cg, A, B, O.PREC_F32, rows)
 
 
+TC = [O.PREC_BF16, O.PREC_TF32]
+TC_SHAPES = [(128, 256, 64), (256, 512, 1024), (1, 1, 1), (3, 5, 7), (129, 257, 100), (300, 1000, 520),
+             (1024, 768, 4096)]
+
+
+@pytest.mark.parametrize("prec", TC)
+@pytest.mark.parametrize("m,n,k", TC_SHAPES)
+def test_tensor_core_within_tolerance(gpu, prec, m, n, k):
+    A, B = _mats(O.MAT_UNIFORM32, 0x5EED, m, k, n)
+    _check(_run_device(prec, A, B), A, B, prec)
+
+
+@pytest.mark.parametrize("prec", TC)
+def test_tensor_core_exact8_bit_exact(gpu, prec):
+    """exact8 operands are exact in bf16 / tf32 and their products are exact
+    in fp32; with |partial sums| < 2^24 ulps the result is order-free."""
+    A, B = _mats(O.MAT_EXACT8, 11, 384, 512, 768)
+    Cg = _run_device(prec, A, B)
+    Cref, _ = O.matmul_f64(A, B)
+    assert np.array_equal(Cg.astype(np.float64), Cref)
+
+
+@pytest.mark.parametrize("prec", TC)
+def test_tensor_core_many_tiles_and_strides(gpu, prec):
+    """More output tiles than SMs (persistent loop, both TMEM buffers) and
+    strided operands."""
+    import torch
+    from paper_1505_05655_b200 import device as D
+    m, n, k = 2304, 4608, 256  # 18 x 18 = 324 tiles > 148 SMs
+    A, B = _mats(O.MAT_UNIFORM32, 13, m, k, n)
+    big_a = torch.zeros(m, k + 8, device="cuda")
+    big_a[:, :k] = torch.from_numpy(A)
+    big_c = torch.full((m, n + 4), -7.0, device="cuda")
+    ws = D.matmul_workspace(prec, m, n, k)
+    D.matmul(prec, big_a[:, :k], torch.from_numpy(B).cuda(), big_c[:, :n], ws)
+    Cg = big_c[:, :n].cpu().numpy()
+    rows = np.arange(0, m, 7).astype(np.uint64)
+    _check(Cg, A, B, prec, rows)
+    assert float(big_c[:, n:].sub(-7.0).abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("prec,name", [(O.PREC_BF16, "bf16"), (O.PREC_TF32, "tf32")])
+def test_gpcx_run_matmul_tensor_core(gpu, prec, name):
+    m, k, n = 200, 300, 400
+    A, B = _mats(O.MAT_UNIFORM32, 21, m, k, n)
+    res, payload = G.run("MATMUL", f"m={m},k={k},n={n},prec={name}", np.concatenate([A.ravel(), B.ravel()]))
+    assert res["prec"] == name
+    _check(payload.view(np.float32).reshape(m, n), A, B, prec)
+
+
 def test_gpcx_run_matmul_f32(gpu):
     m, k, n = 70, 90, 110
     A, B = _mats(O.MAT_UNIFORM32, 5, m, k, n)
