@@ -27,7 +27,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "cuda_util.hpp"
 #include "kernels.hpp"
@@ -46,7 +48,6 @@ constexpr int kThreads = 256;           // 8 warps
 constexpr int kEpiWarp0 = 4;
 constexpr int kTmemCols = 512;          // 2 accumulator buffers x 256 columns
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kGroupM = 16;             // tile raster: 16 m-blocks per group
 
 // ------------------------------------------------------------------ PTX ---
 
@@ -83,7 +84,7 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
   for (;;) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(addr), "r"(parity)
@@ -149,11 +150,11 @@ __device__ __forceinline__ std::uint64_t smem_desc(const void* tile) {
 
 // Instruction descriptor: f32 accumulate, A/B = bf16 (1) or tf32 (2), both
 // K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-template <bool kTf32>
+template <bool kTf32, int kM = BM, int kN = BN>
 __host__ __device__ constexpr std::uint32_t instr_desc() {
   const std::uint32_t fmt = kTf32 ? 2u : 1u;
-  return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<std::uint32_t>(BN >> 3) << 17) |
-         (static_cast<std::uint32_t>(BM >> 4) << 24);
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<std::uint32_t>(kN >> 3) << 17) |
+         (static_cast<std::uint32_t>(kM >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v)[32]) {
@@ -170,13 +171,19 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Tile raster: groups of `group_m` m-blocks swept n-block by n-block, so the
+// tiles resident at once (one wave of persistent CTAs) cover a near-square
+// block of C and read the fewest distinct A / B rows per K step -- the
+// operand panels of a wave come from DRAM once and are L2 hits for every
+// other CTA of the wave.  1-SM 128x256 tiles: 16 x ~9 blocks per wave;
+// CTA-pair 256x256 tiles: 8 x ~9.
 struct TileMap {
-  int mt, nt;
+  int mt, nt, group_m;
   __device__ __forceinline__ void coords(int t, int& mb, int& nb) const {
-    const int per_group = kGroupM * nt;
+    const int per_group = group_m * nt;
     const int g = t / per_group;
-    const int first_m = g * kGroupM;
-    const int gm = min(kGroupM, mt - first_m);
+    const int first_m = g * group_m;
+    const int gm = min(group_m, mt - first_m);
     const int r = t - g * per_group;
     mb = first_m + r % gm;
     nb = r / gm;
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileMap tm{mt, nt};
+  const TileMap tm{mt, nt, 16};
   const int ntiles = mt * nt;
 
   if (warp == 0 && lane == 0) {
@@ -338,6 +345,239 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------- CTA-pair (2-SM) kernel ---
+//
+// Two CTAs of a cluster on a TPC form one 256 x 256 tile: CTA r holds rows
+// [128r, 128r+128) of the A tile and rows [128r, 128r+128) of the B'^T tile
+// (N half) at identical smem offsets; the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 M=256 N=256, which reads both CTAs' smem and
+// writes both CTAs' TMEM (rows 0-127 in the leader, 128-255 in the peer).
+// Per CTA a stage is 32 KiB (half of the 1-SM kernel's B), so the ring is
+// 6 deep for the same smem, and each SM's tensor-core smem reads halve.
+// Barrier protocol (as CUTLASS's 2SM pipeline): both producers wait on
+// their own `empty` slot (the leader's commit multicasts to both CTAs),
+// issue cta_group::2 TMA loads that complete_tx on the LEADER's `full`
+// barrier, and only the leader arms it with the pair's total bytes.  The
+// accumulator-ready commit multicasts to both CTAs' tmem_full; all 8
+// epilogue warps of the pair arrive on the leader's tmem_empty.
+
+constexpr int kStages2 = 7;
+constexpr int kStageBytes2 = 2 * 128 * 128;  // A half + B half, 16 KiB each
+constexpr int kSmemBytes2 = kStages2 * kStageBytes2 + 1024 + 256;
+constexpr std::uint32_t kPeerMask = 0xFEFFFFFFu;  // rank bit of a shared::cluster address
+
+__device__ __forceinline__ std::uint32_t cta_rank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, std::uint32_t leader_bar,
+                                                 void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_pair(std::uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+          "r"(smem_u32(bar)),
+      "h"(static_cast<std::uint16_t>(0x3))
+      : "memory");
+}
+
+template <bool kTf32>
+__device__ __forceinline__ void tc_mma_pair(std::uint32_t tmem_d, std::uint64_t adesc,
+                                            std::uint64_t bdesc, std::uint32_t idesc,
+                                            std::uint32_t accumulate) {
+  if constexpr (kTf32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// Arrive on the cluster leader's copy of a barrier (same smem offset).
+__device__ __forceinline__ void mbar_arrive_leader(std::uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool kTf32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 float* __restrict__ C, int m, int n, std::uint64_t ldc, int ktiles, int mt, int nt) {
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+      (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~static_cast<std::uintptr_t>(1023));
+  std::uint8_t* tiles = smem;
+  auto* bars = reinterpret_cast<std::uint64_t*>(smem + kStages2 * kStageBytes2);
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + kStages2;
+  std::uint64_t* tmem_full = bars + 2 * kStages2;
+  std::uint64_t* tmem_empty = tmem_full + 2;
+  auto* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const TileMap tm{mt, nt, 8};  // 256 x 256 tiles
+  const int ntiles = mt * nt;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const std::uint32_t a_row0 = rank * 128;
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int mb, nb;
+        tm.coords(t, mb, nb);
+        for (int kb = 0; kb < ktiles; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          std::uint8_t* sa = tiles + stage * kStageBytes2;
+          const std::uint32_t leader_full = smem_u32(&full[stage]) & kPeerMask;
+          if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes2);
+          const int kx = kb * (kTf32 ? 32 : 64);
+          tma_load_2d_pair(&map_a, leader_full, sa, kx, mb * 256 + a_row0);
+          tma_load_2d_pair(&map_b, leader_full, sa + 128 * 128, kx, nb * 256 + a_row0);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr std::uint32_t idesc = instr_desc<kTf32, 256, 256>();
+      int stage = 0;
+      std::uint32_t phase = 0;
+      int acc = 0;
+      std::uint32_t acc_phase = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const std::uint32_t tmem_d = tmem_base + static_cast<std::uint32_t>(acc * 256);
+        for (int kb = 0; kb < ktiles; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const std::uint8_t* sa = tiles + stage * kStageBytes2;
+          const std::uint64_t adesc = smem_desc(sa);
+          const std::uint64_t bdesc = smem_desc(sa + 128 * 128);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_pair<kTf32>(tmem_d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          tc_commit_pair(&empty[stage]);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&tmem_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    const int quarter = warp - kEpiWarp0;
+    int acc = 0;
+    std::uint32_t acc_phase = 0;
+    const bool vec_ok = (ldc % 4 == 0) && ((reinterpret_cast<std::uintptr_t>(C) & 15) == 0);
+    for (int t = pair; t < ntiles; t += npairs) {
+      int mb, nb;
+      tm.coords(t, mb, nb);
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
+      float* crow = C + static_cast<std::uint64_t>(row) * ldc;
+      const std::uint32_t taddr = tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                                  static_cast<std::uint32_t>(acc * 256);
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        std::uint32_t v[32];
+        tmem_ld32(taddr + c, v);
+        const int col = nb * 256 + c;
+        if (row < m) {
+          if (vec_ok && col + 32 <= n) {
+            float4* dst = reinterpret_cast<float4*>(crow + col);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < n) crow[col + j] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------ operand prep ---
 
 __device__ __forceinline__ float round_tf32(float x) {
@@ -430,6 +670,21 @@ std::uint64_t k_pad(int prec, std::uint64_t k) {
 
 std::uint64_t align256(std::uint64_t x) { return (x + 255) & ~255ull; }
 
+// CTA-pair kernel for problems with enough 256 x 256 tiles to fill the
+// SM pairs; the 1-SM 128 x 256 kernel for small / skinny ones.  The
+// GPCX_TC_KERNEL=1sm|2sm override exists for tests and A/B measurements.
+bool use_pair_kernel(std::uint64_t m, std::uint64_t n, std::uint64_t k, int sms) {
+  const char* force = std::getenv("GPCX_TC_KERNEL");
+  if (force != nullptr && std::string(force) == "1sm") return false;
+  if (force != nullptr && std::string(force) == "2sm") return true;
+  // Measured on B200 (tools/c4_ab.py, profiles/): the pair kernel wins at
+  // K <= 8192 (1115 vs 1039 TFLOP/s at 8192^3); at K = 32768 its operand
+  // panels hit L2 less (10.6 vs 4.6 GB of DRAM reads on 8192x8192x32768),
+  // the extra HBM power lowers the capped clock and the 1-SM kernel wins.
+  const std::uint64_t tiles2 = ((m + 255) / 256) * ((n + 255) / 256);
+  return m >= 256 && k <= 8192 && tiles2 >= static_cast<std::uint64_t>(sms / 2);
+}
+
 }  // namespace
 
 std::uint64_t tc_workspace_bytes(int prec, std::uint64_t m, std::uint64_t n, std::uint64_t k) {
@@ -469,10 +724,25 @@ void launch_tc(int prec, std::uint64_t m, std::uint64_t n, std::uint64_t k, cons
     GPCX_LAUNCH_CHECK();
   }
 
+  const int ktiles = static_cast<int>(kp / (tf32 ? 32 : 64));
+  if (use_pair_kernel(m, n, k, sms)) {
+    const CUtensorMap ma = make_map(a_p, tf32, m, kp, 128);
+    const CUtensorMap mb = make_map(b_p, tf32, n, kp, 128);
+    const int mt = static_cast<int>((m + 255) / 256), nt = static_cast<int>((n + 255) / 256);
+    const int grid = 2 * std::min(mt * nt, sms / 2);
+    if (tf32) {
+      GPCX_CUDA(cudaFuncSetAttribute(gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2));
+      gemm2_kernel<true><<<grid, kThreads, kSmemBytes2, stream>>>(ma, mb, C, (int)m, (int)n, ldc, ktiles, mt, nt);
+    } else {
+      GPCX_CUDA(cudaFuncSetAttribute(gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2));
+      gemm2_kernel<false><<<grid, kThreads, kSmemBytes2, stream>>>(ma, mb, C, (int)m, (int)n, ldc, ktiles, mt, nt);
+    }
+    GPCX_LAUNCH_CHECK();
+    return;
+  }
   const CUtensorMap ma = make_map(a_p, tf32, m, kp, BM);
   const CUtensorMap mb = make_map(b_p, tf32, n, kp, BN);
   const int mt = static_cast<int>((m + BM - 1) / BM), nt = static_cast<int>((n + BN - 1) / BN);
-  const int ktiles = static_cast<int>(kp / (tf32 ? 32 : 64));
   const int grid = std::min(mt * nt, sms);
   if (tf32) {
     GPCX_CUDA(cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));

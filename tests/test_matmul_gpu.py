@@ -101,15 +101,22 @@ TC_SHAPES = [(128, 256, 64), (256, 512, 1024), (1, 1, 1), (3, 5, 7), (129, 257, 
              (1024, 768, 4096)]
 
 
+@pytest.fixture(params=["1sm", "2sm"])
+def tc_kernel(request, monkeypatch):
+    """Runs a test on the 1-SM (128x256) and the CTA-pair (256x256) kernel."""
+    monkeypatch.setenv("GPCX_TC_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("prec", TC)
 @pytest.mark.parametrize("m,n,k", TC_SHAPES)
-def test_tensor_core_within_tolerance(gpu, prec, m, n, k):
+def test_tensor_core_within_tolerance(gpu, tc_kernel, prec, m, n, k):
     A, B = _mats(O.MAT_UNIFORM32, 0x5EED, m, k, n)
     _check(_run_device(prec, A, B), A, B, prec)
 
 
 @pytest.mark.parametrize("prec", TC)
-def test_tensor_core_exact8_bit_exact(gpu, prec):
+def test_tensor_core_exact8_bit_exact(gpu, tc_kernel, prec):
     """exact8 operands are exact in bf16 / tf32 and their products are exact
     in fp32; with |partial sums| < 2^24 ulps the result is order-free."""
     A, B = _mats(O.MAT_EXACT8, 11, 384, 512, 768)
@@ -119,7 +126,18 @@ def test_tensor_core_exact8_bit_exact(gpu, prec):
 
 
 @pytest.mark.parametrize("prec", TC)
-def test_tensor_core_many_tiles_and_strides(gpu, prec):
+def test_tensor_core_kernels_agree_bitwise(gpu, prec, monkeypatch):
+    """Same K order per output in both kernels -> identical bits."""
+    A, B = _mats(O.MAT_UNIFORM32, 17, 1000, 1500, 700)
+    monkeypatch.setenv("GPCX_TC_KERNEL", "1sm")
+    c1 = _run_device(prec, A, B)
+    monkeypatch.setenv("GPCX_TC_KERNEL", "2sm")
+    c2 = _run_device(prec, A, B)
+    assert np.array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("prec", TC)
+def test_tensor_core_many_tiles_and_strides(gpu, tc_kernel, prec):
     """More output tiles than SMs (persistent loop, both TMEM buffers) and
     strided operands."""
     import torch

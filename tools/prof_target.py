@@ -1,0 +1,58 @@
+"""Short, deterministic workload for ncu captures (one launch of each hot
+kernel at the bench configuration):
+  LUT_CORRECT equalize on the C3 scene (32768^2 u16): hist, merge, from_hist, apply
+  MATMUL bf16 8192^3 (and tf32 4096^3) through the tcgen05 path
+    ncu --set full -k regex:'hist_kernel|apply_kernel|gemm_kernel' ... python tools/prof_target.py
+"""
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="lut,mm")
+    ap.add_argument("--mm", type=int, default=8192)
+    args = ap.parse_args()
+    import torch
+    from paper_1505_05655_b200 import device as D
+    if "lut" in args.what:
+        n = 32768 * 32768
+        img = D.synth_image(0, 0x5EED, 32768, 32768)
+        out = torch.empty_like(img)
+        lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+        D.lut_correct(img, out, 0, lut, stats, ws)
+        torch.cuda.synchronize()
+        del img, out
+    if "longk" in args.what:  # C4-like long K, cheaper to replay than 32768^3
+        import os
+        m = n = 8192
+        k = 32768
+        A = D.synth_matrix(1, 1, m, k)
+        B = D.synth_matrix(1, 2, k, n)
+        Cm = torch.empty(m, n, device="cuda")
+        ws = D.matmul_workspace(2, m, n, k)
+        for kern in ("1sm", "2sm"):
+            os.environ["GPCX_TC_KERNEL"] = kern
+            D.matmul(2, A, B, Cm, ws)
+            torch.cuda.synchronize()
+        print("done")
+        return
+    if "mm" in args.what:
+        s = args.mm
+        A = D.synth_matrix(1, 1, s, s)
+        B = D.synth_matrix(1, 2, s, s)
+        Cm = torch.empty(s, s, device="cuda")
+        for prec in (2, 1):
+            ws = D.matmul_workspace(prec, s, s, s)
+            D.matmul(prec, A, B, Cm, ws)
+            torch.cuda.synchronize()
+    print("done")
+
+
+if __name__ == "__main__":
+    main()
