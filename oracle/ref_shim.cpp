@@ -64,13 +64,34 @@ struct LutArgs {
   int mode;
 };
 
-LutArgs lut_args(const wire::ParamMap& p, bool has_mode) {
-  LutArgs a{p.get_uint("rows"), p.get_uint("cols"), ORC_LUT_EQUALIZE};
-  if (a.rows == 0) fail(Errc::BadValue, "rows must be positive");
-  if (a.cols == 0) fail(Errc::BadValue, "cols must be positive");
-  if (a.rows > wire::kMaxPayload || a.cols > wire::kMaxPayload)
+// The sizing rules and messages of the product's task_spec.cpp, written
+// against the reference's own ParamMap: the reference's dim_product()
+// (proj/src/wire.cpp:67-80) is file-local, so it is restated here.
+std::uint64_t dims(const char* ak, std::uint64_t a, const char* bk, std::uint64_t b,
+                   std::uint64_t scale) {
+  if (a == 0) fail(Errc::BadValue, std::string(ak) + " must be positive");
+  if (b == 0) fail(Errc::BadValue, std::string(bk) + " must be positive");
+  if (a > wire::kMaxPayload || b > wire::kMaxPayload)
     fail(Errc::Overflow, "dimension exceeds payload cap");
-  if (a.rows * a.cols * 2 > wire::kMaxPayload) fail(Errc::Overflow, "payload exceeds cap");
+  const std::uint64_t len = a * b * scale;
+  if (len > wire::kMaxPayload)
+    fail(Errc::Overflow, "payload length " + std::to_string(len) + " exceeds cap " +
+                             std::to_string(wire::kMaxPayload));
+  return len;
+}
+
+std::uint64_t capped(std::uint64_t a, std::uint64_t b) {
+  const std::uint64_t len = a + b;
+  if (len > wire::kMaxPayload)
+    fail(Errc::Overflow, "payload length " + std::to_string(len) + " exceeds cap " +
+                             std::to_string(wire::kMaxPayload));
+  return len;
+}
+
+LutArgs lut_args(const wire::ParamMap& p, bool has_mode) {
+  LutArgs a{p.get_uint("rows"), 0, ORC_LUT_EQUALIZE};
+  a.cols = p.get_uint("cols");
+  dims("rows", a.rows, "cols", a.cols, 2);
   const std::string dtype = p.get_or("dtype", "u16");
   if (dtype != "u16") fail(Errc::BadValue, "dtype=" + dtype);
   if (has_mode) {
@@ -87,14 +108,13 @@ struct MatArgs {
 };
 
 MatArgs mat_args(const wire::ParamMap& p) {
-  MatArgs a{p.get_uint("m"), p.get_uint("k"), p.get_uint("n"), ORC_PREC_F32};
-  for (auto [key, v] : {std::pair<const char*, std::uint64_t>{"m", a.m}, {"k", a.k}, {"n", a.n}})
-    if (v == 0) fail(Errc::BadValue, std::string(key) + " must be positive");
-  if (a.m > wire::kMaxPayload || a.k > wire::kMaxPayload || a.n > wire::kMaxPayload)
-    fail(Errc::Overflow, "dimension exceeds payload cap");
-  if (a.m * a.k * 4 > wire::kMaxPayload || a.k * a.n * 4 > wire::kMaxPayload ||
-      a.m * a.k * 4 + a.k * a.n * 4 > wire::kMaxPayload || a.m * a.n * 4 > wire::kMaxPayload)
-    fail(Errc::Overflow, "payload exceeds cap");
+  MatArgs a{p.get_uint("m"), 0, 0, ORC_PREC_F32};
+  a.k = p.get_uint("k");
+  a.n = p.get_uint("n");
+  const std::uint64_t la = dims("m", a.m, "k", a.k, 4);
+  const std::uint64_t lb = dims("k", a.k, "n", a.n, 4);
+  capped(la, lb);
+  dims("m", a.m, "n", a.n, 4);
   const std::string prec = p.get_or("prec", "f32");
   if (prec == "tf32") a.prec = ORC_PREC_TF32;
   else if (prec == "bf16") a.prec = ORC_PREC_BF16;
@@ -134,9 +154,7 @@ void add_oracle_tasks(task::TaskRegistry& r) {
          .required_params = {"rows", "cols"},
          .payload_rule = [](const wire::ParamMap& p) {
            const LutArgs a = lut_args(p, false);
-           const std::uint64_t len = kLutBytes + a.rows * a.cols * 2;
-           if (len > wire::kMaxPayload) fail(Errc::Overflow, "payload exceeds cap");
-           return len;
+           return capped(kLutBytes, a.rows * a.cols * 2);
          },
          .handler = [](const wire::ParamMap& p, std::span<const std::uint8_t> in) {
            const LutArgs a = lut_args(p, false);

@@ -2,6 +2,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "../cuda_util.hpp"
@@ -179,6 +180,7 @@ PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
     this->~PinnedLease();
     ptr_ = o.ptr_;
     cap_ = o.cap_;
+    pageable_ = o.pageable_;
     o.ptr_ = nullptr;
   }
   return *this;
@@ -186,6 +188,11 @@ PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
 
 PinnedLease::~PinnedLease() {
   if (ptr_ == nullptr) return;
+  if (pageable_) {
+    std::free(ptr_);
+    ptr_ = nullptr;
+    return;
+  }
   PinnedPool& pool = pinned_pool();
   std::lock_guard<std::mutex> lock(pool.mu);
   if (pool.idle_bytes + cap_ > kPinnedIdleCap) {
@@ -213,7 +220,12 @@ PinnedLease pinned_acquire(std::uint64_t bytes) {
     }
   }
   void* p = nullptr;
-  GPCX_CUDA(cudaHostAlloc(&p, cls, cudaHostAllocPortable));
+  if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    p = std::malloc(cls);
+    if (p == nullptr) fail(Errc::TaskFailed, "out of host memory");
+    return PinnedLease(p, cls, /*pageable=*/true);
+  }
   return PinnedLease(p, cls);
 }
 

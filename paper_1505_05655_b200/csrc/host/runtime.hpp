@@ -120,8 +120,11 @@ bool is_pinned(const void* p);
 class PinnedLease {
  public:
   PinnedLease() = default;
-  PinnedLease(void* p, std::uint64_t cap) : ptr_(p), cap_(cap) {}
-  PinnedLease(PinnedLease&& o) noexcept : ptr_(o.ptr_), cap_(o.cap_) { o.ptr_ = nullptr; }
+  PinnedLease(void* p, std::uint64_t cap, bool pageable = false)
+      : ptr_(p), cap_(cap), pageable_(pageable) {}
+  PinnedLease(PinnedLease&& o) noexcept : ptr_(o.ptr_), cap_(o.cap_), pageable_(o.pageable_) {
+    o.ptr_ = nullptr;
+  }
   PinnedLease& operator=(PinnedLease&& o) noexcept;
   PinnedLease(const PinnedLease&) = delete;
   ~PinnedLease();
@@ -131,7 +134,10 @@ class PinnedLease {
  private:
   void* ptr_ = nullptr;
   std::uint64_t cap_ = 0;
+  bool pageable_ = false;  // page-locking unavailable (no usable device)
 };
+// A pooled pinned buffer; when page-locking fails (no usable device) a plain
+// heap buffer, so framing still works and the handler reports the GPU error.
 PinnedLease pinned_acquire(std::uint64_t bytes);
 void pinned_trim();  // frees idle pooled buffers
 

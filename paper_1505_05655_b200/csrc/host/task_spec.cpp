@@ -61,8 +61,9 @@ MatmulParams parse_matmul(const wire::ParamMap& params) {
   p.m = params.get_uint("m");
   p.k = params.get_uint("k");
   p.n = params.get_uint("n");
-  wire::capped_sum(wire::dim_product("m", p.m, "k", p.k, 4),
-                   wire::dim_product("k", p.k, "n", p.n, 4));
+  const std::uint64_t a_bytes = wire::dim_product("m", p.m, "k", p.k, 4);
+  const std::uint64_t b_bytes = wire::dim_product("k", p.k, "n", p.n, 4);
+  wire::capped_sum(a_bytes, b_bytes);
   wire::dim_product("m", p.m, "n", p.n, 4);  // the response must fit too
   const std::string prec = params.get_or("prec", "f32");
   if (prec == "f32") p.prec = GPCX_PREC_F32;

@@ -1,0 +1,150 @@
+"""The B200 task server over loopback TCP, driven by the REFERENCE client
+(client::submit compiled from /root/reference/proj/src/client.cpp into
+oracle/_ref) -- the client a user of the reference already has.
+
+Mirrors proj/tests/test_server.cpp:190-386 (ephemeral port, concurrent
+clients, idle timeout, abandoned connection, port in use) and
+acceptance.cpp:446-523 (served bytes == direct kernel bytes), with the
+reference server (same registry, CPU-restated tasks) as the comparison.
+"""
+from __future__ import annotations
+
+import socket
+import threading
+import time
+
+import numpy as np
+import pytest
+
+import paper_1505_05655_b200 as G
+import wire_util as W
+
+
+@pytest.fixture(scope="module")
+def server():
+    with G.Server(max_tasks=4, idle_timeout_ms=300) as s:
+        yield s
+
+
+def test_ephemeral_port_and_early_errors_match_reference(server, refl):
+    assert server.port != 0
+    with refl.RefServer() as rs:
+        for flag, params in [("NOPE", "rows=4,cols=4"), ("LUT_CORRECT", "rows=4"),
+                             ("LUT_CORRECT", "rows=q,cols=4"), ("MATMUL", "m=1,k=1,n=1,prec=x"),
+                             ("LUT_CORRECT", "rows=32768,cols=32768")]:
+            ours = refl.ref_submit(server.port, flag, params, b"\x01\x02", "x.bin")
+            ref = refl.ref_submit(rs.port, flag, params, b"\x01\x02", "x.bin")
+            assert ours == ref
+            assert ours[0].startswith("ERR:")
+
+
+def test_raw_bad_header_gets_error_and_salvaged_name(server, refl):
+    req = W.header("\x07AD", "", name="keep.me")
+    resp = W.parse_response(W.roundtrip(server.port, req))
+    assert resp["status"] == "ERR:BAD_HEADER" and resp["name"] == "keep.me"
+    with refl.RefServer() as rs:
+        assert W.roundtrip(server.port, req) == W.roundtrip(rs.port, req)
+
+
+def test_early_reject_without_payload(server):
+    """Header promising 2 GiB: the answer comes before any payload is sent."""
+    with socket.create_connection(("127.0.0.1", server.port), timeout=10) as s:
+        s.sendall(W.header("LUT_CORRECT", "rows=32768,cols=32768", has_payload=True))
+        data = s.recv(4096)
+    assert W.parse_response(data)["status"] == "ERR:TOO_LARGE"
+
+
+def test_idle_connection_is_dropped_without_response(server):
+    with socket.create_connection(("127.0.0.1", server.port), timeout=10) as s:
+        s.sendall(W.header("LUT_CORRECT", "rows=64,cols=64", has_payload=True) + b"\0" * 100)
+        t0 = time.time()
+        data = s.recv(4096)  # server closes after its 300 ms idle timeout
+        assert data == b"" and time.time() - t0 < 5
+
+
+def test_abandoned_connection_does_not_wedge_server(server, refl):
+    s = socket.create_connection(("127.0.0.1", server.port))
+    s.sendall(b"LUT")
+    s.close()
+    status, _, _, _ = refl.ref_submit(server.port, "NOPE", "", b"", "a")
+    assert status == "ERR:UNKNOWN_TASK"
+
+
+def test_port_in_use_fails_with_bind_failed(server):
+    with pytest.raises(G.GpcxError) as e:
+        G.Server(port=server.port).start()
+    assert e.value.code == "BindFailed"
+
+
+def test_concurrent_clients(server, refl):
+    results = []
+
+    def worker(i):
+        results.append(refl.ref_submit(server.port, "NOPE", f"i={i}", b"", f"n{i}"))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(16)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert len(results) == 16 and all(r[0] == "ERR:UNKNOWN_TASK" for r in results)
+    assert sorted(r[3] for r in results) == sorted(f"n{i}" for i in range(16))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["equalize", "stretch"])
+def test_loopback_lut_correct_equals_reference_server(gpu, server, refl, mode):
+    from oracle import oracle as O
+    rows, cols = 1024, 1536
+    img = O.synth_image(O.IMG_RAMP12, 0x5EED, rows, cols)
+    params = f"rows={rows},cols={cols},mode={mode}"
+    ours = refl.ref_submit(server.port, "LUT_CORRECT", params, img.tobytes(), "c.raw")
+    with refl.RefServer() as rs:
+        ref = refl.ref_submit(rs.port, "LUT_CORRECT", params, img.tobytes(), "c.raw")
+    assert ours[0] == "OK" and ours == ref
+    direct_out, _, _ = O.lut_correct(img, O.LUT_EQUALIZE if mode == "equalize" else O.LUT_STRETCH)
+    assert ours[2] == direct_out.tobytes()
+
+
+@pytest.mark.gpu
+def test_loopback_matmul_tensor_core(gpu, server, refl):
+    from oracle import oracle as O
+    m, k, n = 96, 200, 128
+    A = O.synth_matrix(O.MAT_UNIFORM32, 2, m, k)
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(2), k, n)
+    payload = A.tobytes() + B.tobytes()
+    status, params, data, name = refl.ref_submit(server.port, "MATMUL", f"m={m},k={k},n={n},prec=bf16",
+                                                 payload, "c.f32")
+    assert status == "OK" and name == "c.f32"
+    assert G.parse_params(params) == {"m": str(m), "n": str(n), "k": str(k), "prec": "bf16",
+                                      "bytes": str(m * n * 4)}
+    Cg = np.frombuffer(data, dtype=np.float32).reshape(m, n)
+    Cref, ab = O.matmul_f64(O.round_matrix(O.PREC_BF16, A), O.round_matrix(O.PREC_BF16, B))
+    assert np.all(np.abs(Cg - Cref) <= 1e-5 * ab)
+
+
+@pytest.mark.gpu
+def test_many_concurrent_gpu_requests(gpu, server, refl):
+    """The config-C5 shape in miniature: 16 concurrent clients, each a
+    LUT_GEN -> LUT_APPLY -> MATMUL chain, against the 4-worker server."""
+    from oracle import oracle as O
+    errors = []
+
+    def chain(i):
+        try:
+            img = O.synth_image(O.IMG_UNIFORM16, i, 128, 128)
+            st, p, lut, _ = refl.ref_submit(server.port, "LUT_GEN", "rows=128,cols=128", img.tobytes())
+            assert st == "OK"
+            st, p, out, _ = refl.ref_submit(server.port, "LUT_APPLY", "rows=128,cols=128", lut + img.tobytes())
+            assert st == "OK"
+            r_out, _, _ = O.lut_correct(img, O.LUT_EQUALIZE)
+            assert out == r_out.tobytes()
+            x = np.frombuffer(out, dtype=np.uint16).astype(np.float32).reshape(128, 128) / 65535
+            st, p, c, _ = refl.ref_submit(server.port, "MATMUL", "m=128,k=128,n=128",
+                                          x.tobytes() + x.tobytes())
+            assert st == "OK"
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=chain, args=(i,)) for i in range(16)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errors, errors
