@@ -343,7 +343,89 @@ def matmul_e2e_leg(steps: int) -> dict:
             "d2h_bytes_per_step": nb}
 
 
+# ------------------------------------------------------------------ C5 ---
+
+# Chain sizes: the C1 image (4096^2 u16) and the C2 product (4096^3), so each
+# chain is LUT_GEN + LUT_APPLY of C1 and a MATMUL of the corrected image
+# (as f32 in [0,1]) with B -- 290 MB over TCP and 137 GFLOP per chain.
+C5_IMG = 4096
+C5_MM = 4096
+C5_REQUESTS = 64
+C5_CPU_SAMPLE = 16  # chains timed on the reference CPU server (bounded sample)
+
+
+def c5_inputs() -> tuple[list[bytes], bytes]:
+    from paper_1505_05655_b200 import device as D
+    imgs = [D.synth_image(0, SEED + i, C5_IMG, C5_IMG).cpu().numpy().view(np.uint16).tobytes()
+            for i in range(C5_REQUESTS)]
+    B = D.synth_matrix(1, SEED_B, C5_MM, C5_MM).cpu().numpy().tobytes()
+    return imgs, B
+
+
+def c5_chain(port: int, img: bytes, B: bytes, prec: str) -> int:
+    """LUT_GEN -> LUT_APPLY (image correction) -> MATMUL on the corrected
+    image's top-left 1024^2 block; returns the bytes moved over TCP."""
+    from paper_1505_05655_b200.client import submit
+    dims = f"rows={C5_IMG},cols={C5_IMG}"
+    r1 = submit("127.0.0.1", port, "LUT_GEN", dims, img, "lut.bin")
+    assert r1.ok, r1.status
+    r2 = submit("127.0.0.1", port, "LUT_APPLY", dims, [r1.payload, img], "img.raw")
+    assert r2.ok, r2.status
+    corr = np.frombuffer(r2.payload, dtype=np.uint16).reshape(C5_IMG, C5_IMG)
+    A = corr[:C5_MM, :C5_MM].astype(np.float32)
+    A *= np.float32(1.0 / 65535.0)
+    r3 = submit("127.0.0.1", port, "MATMUL", f"m={C5_MM},k={C5_MM},n={C5_MM},prec={prec}", [A, B], "c.f32")
+    assert r3.ok, r3.status
+    return (len(img) * 2 + len(r1.payload) + A.nbytes + len(B) + len(r1.payload) + len(r2.payload)
+            + len(r3.payload) + 6 * 260)
+
+
+def c5_run(port: int, imgs, B, prec: str, clients: int = C5_REQUESTS) -> dict:
+    """All chains submitted at once by `clients` client threads (queued at
+    the server, which runs max_tasks of them concurrently)."""
+    import concurrent.futures as cf
+    t = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=clients) as ex:
+        moved = sum(ex.map(lambda im: c5_chain(port, im, B, prec), imgs))
+    s = time.perf_counter() - t
+    return {"chains": len(imgs), "chains_per_s": len(imgs) / s, "requests_per_s": 3 * len(imgs) / s,
+            "seconds": s, "tcp_bytes": moved}
+
+
+def c5_leg(n_gpus: int) -> dict:
+    """Config C5: 64 queued client requests, each the chain LUT_GEN ->
+    LUT_APPLY -> MATMUL, against the B200 task server (N GPUs bound in one
+    server process, requests round-robined over them)."""
+    import paper_1505_05655_b200 as G
+    imgs, B = c5_inputs()
+    G.init(list(range(n_gpus)))
+    try:
+        with G.Server(max_tasks=0) as srv:
+            c5_run(srv.port, imgs[:8], B, "bf16")  # warm-up: slots, pinned pools
+            res = c5_run(srv.port, imgs, B, "bf16")
+    finally:
+        G.init([0])
+    res.update({"workload": f"C5: {C5_REQUESTS} concurrent clients x (LUT_GEN -> LUT_APPLY -> "
+                            f"MATMUL prec=bf16), {C5_IMG}^2 u16 images, {C5_MM}^3 matmul",
+                "server": "gpcx B200 server (max_tasks = 2 x hw threads), loopback TCP, "
+                          "Python wire client"})
+    return res
+
+
 # -------------------------------------------------------------- CPU legs ---
+
+def cpu_c5() -> dict:
+    """C5 against the reference server (the reference's own TCP / dispatch
+    code, proj/src/server.cpp) serving the CPU-restated tasks."""
+    from oracle import oracle as O
+    imgs, B = c5_inputs()
+    with O.RefServer(max_tasks=0) as rs:
+        res = c5_run(rs.port, imgs[:C5_CPU_SAMPLE], B, "bf16", C5_CPU_SAMPLE)
+    res.update({"kind": "port", "cores": O.max_threads(),
+                "sample": f"the first {C5_CPU_SAMPLE} chains of the same corpus, {C5_CPU_SAMPLE} concurrent "
+                          "clients, through the reference server "
+                          "(oracle/_ref: reference server + restated CPU kernels)"})
+    return res
 
 def cpu_lut(mode: int, sample_rows: int = 4096, reps: int = 3) -> dict:
     """The restated oracle (kind "port") on a row-band sample of the C3
@@ -469,6 +551,11 @@ def run_b200(args) -> None:
         if d.n == 1:
             mm_line["cpu_baseline"] = cpu_matmul()
         line.setdefault("matmul", {})["c2_f32"] = mm_line
+    if args.workload in ("all", "c5"):
+        c5 = c5_leg(d.n)
+        if d.n == 1:
+            c5["cpu_baseline"] = cpu_c5()
+        line["c5"] = c5
     print(json.dumps(line), flush=True)
 
 
@@ -511,7 +598,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["all", "lut", "matmul"], default="all")
+    ap.add_argument("--workload", choices=["all", "lut", "matmul", "c5"], default="all")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <exception>
 #include <future>
@@ -38,10 +39,21 @@ struct Band {
   std::uint64_t row0, nrows;
 };
 
+// Requests currently executing in this process.  With several in flight
+// the devices are already busy with other requests, so each request runs
+// whole on one device (replicas, round robin) instead of being sharded.
+std::atomic<int> g_inflight{0};
+
+struct InflightGuard {
+  InflightGuard() { g_inflight.fetch_add(1); }
+  ~InflightGuard() { g_inflight.fetch_sub(1); }
+};
+
 std::vector<Band> plan_bands(std::uint64_t rows, std::uint64_t work, std::uint64_t threshold) {
   rt::Runtime& R = rt::Runtime::get();
   const int ndev = R.ndev();
-  if (ndev <= 1 || work < threshold || rows < 2) return {Band{R.pick_device_index(), 0, rows}};
+  if (ndev <= 1 || work < threshold || rows < 2 || g_inflight.load() > 1)
+    return {Band{R.pick_device_index(), 0, rows}};
   const std::uint64_t g = std::min<std::uint64_t>(static_cast<std::uint64_t>(ndev), rows);
   const std::uint64_t per = (rows + g - 1) / g;
   std::vector<Band> bands;
@@ -86,6 +98,7 @@ void for_each_band(std::size_t count, Fn&& fn) {
 gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t* img_in,
                         const std::uint16_t* lut_in, std::uint16_t* out_px,
                         std::uint16_t* lut_out) {
+  const InflightGuard inflight;
   const std::uint64_t n = p.pixels();
   const auto* img = reinterpret_cast<const std::uint8_t*>(img_in);
   auto* outb = reinterpret_cast<std::uint8_t*>(out_px);
@@ -188,6 +201,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
 }
 
 void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* Cout) {
+  const InflightGuard inflight;
   auto* outb = reinterpret_cast<std::uint8_t*>(Cout);
   const std::vector<Band> bands = plan_bands(p.m, 2 * p.m * p.n * p.k, kShardMinFlops);
   const std::size_t G = bands.size();

@@ -1,0 +1,81 @@
+"""The N>1 path on CPU: world_size 2 (and 3) over gloo, one process per
+rank, running paper_1505_05655_b200.shard's exchange logic with the CPU
+oracle as the per-band compute.  The sharded result must equal the
+single-process oracle bit-for-bit (the parexec invariance contract carried
+to ranks)."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1505_05655_b200.shard import ShardedLut, band, bands, gather_bands
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_band_partition_covers_rows_once():
+    for rows in (1, 2, 7, 32768, 4099):
+        for n in (1, 2, 3, 4, 8):
+            bs = bands(rows, n)
+            covered = [r for r0, nr in bs for r in range(r0, r0 + nr)]
+            assert covered == list(range(rows))
+            assert band(rows, n, n - 1)[0] + band(rows, n, n - 1)[1] <= rows
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, rows, cols, mode, q):
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r0, nr = band(rows, world, rank)
+    img = torch.from_numpy(O.synth_image(O.IMG_UNIFORM16 if mode else O.IMG_RAMP12, 7, rows, cols, r0, nr)
+                           .astype(np.int64))
+
+    def hist(b):
+        return torch.from_numpy(O.lut_hist(b.numpy().astype(np.uint16)).astype(np.int64))
+
+    def lut_from_hist(h):
+        return O.lut_from_hist(h.numpy().astype(np.uint64), mode)
+
+    def apply(lut, b):
+        return torch.from_numpy(lut[b.numpy()].astype(np.int64))
+
+    out, lut, stats = ShardedLut(dist, hist, lut_from_hist, apply).run(img)
+    full = gather_bands(dist, out, [nr_ for _, nr_ in bands(rows, world)], cols)
+    if rank == 0:
+        q.put((full.numpy().astype(np.uint16).tobytes(), lut.tobytes(), stats))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mode", [(2, 0), (2, 1), (3, 0)])
+def test_sharded_lut_correct_over_gloo_equals_single_process(world, mode):
+    from oracle import oracle as O
+    rows, cols = 301, 173  # ragged bands
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, rows, cols, mode, q)) for r in range(world)]
+    [p.start() for p in procs]
+    out, lut, stats = q.get(timeout=120)
+    [p.join(timeout=60) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    img = O.synth_image(O.IMG_UNIFORM16 if mode else O.IMG_RAMP12, 7, rows, cols)
+    r_out, r_lut, r_st = O.lut_correct(img, mode)
+    assert out == r_out.tobytes()
+    assert lut == r_lut.tobytes()
+    assert stats == r_st
