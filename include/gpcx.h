@@ -176,9 +176,11 @@ int gpcx_lut_workspace_size(uint64_t n, uint64_t* bytes);
 /* 65536-bin u32 histogram of n u16 samples (n < 2^32). */
 int gpcx_lut_hist_device(const uint16_t* img, uint64_t n, uint32_t* hist,
                          void* ws, uint64_t ws_bytes, void* stream);
-/* LUT (65536 x u16) + stats from a histogram (stats: device pointer). */
+/* LUT (65536 x u16) + stats from a histogram (stats: device pointer); ws is
+ * a LUT workspace (scratch for the cooperative build kernel). */
 int gpcx_lut_from_hist_device(const uint32_t* hist, int mode, uint16_t* lut,
-                              gpcx_lut_stats* stats, void* stream);
+                              gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
+                              void* stream);
 /* min/max statistics only (stretch mode's reduction); stats device ptr. */
 int gpcx_lut_minmax_device(const uint16_t* img, uint64_t n,
                            gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,

@@ -83,7 +83,7 @@ def _load() -> C.CDLL:
         "gpcx_pinned_free": ([vp], None),
         "gpcx_lut_workspace_size": ([u64, pu64], i32),
         "gpcx_lut_hist_device": ([vp, u64, vp, vp, u64, vp], i32),
-        "gpcx_lut_from_hist_device": ([vp, i32, vp, vp, vp], i32),
+        "gpcx_lut_from_hist_device": ([vp, i32, vp, vp, vp, u64, vp], i32),
         "gpcx_lut_minmax_device": ([vp, u64, vp, vp, u64, vp], i32),
         "gpcx_lut_from_minmax_device": ([vp, vp, vp], i32),
         "gpcx_lut_gen_device": ([vp, u64, i32, vp, vp, vp, u64, vp], i32),

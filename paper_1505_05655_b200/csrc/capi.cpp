@@ -230,11 +230,13 @@ int gpcx_lut_hist_device(const uint16_t* img, uint64_t n, uint32_t* hist, void* 
 }
 
 int gpcx_lut_from_hist_device(const uint32_t* hist, int mode, uint16_t* lut,
-                              gpcx_lut_stats* stats, void* stream) {
+                              gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
+                              void* stream) {
   return guarded([&] {
     if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
       gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
-    gpcx::lut::launch_from_hist(hist, mode, lut, stats, as_stream(stream));
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    gpcx::lut::launch_from_hist(hist, mode, lut, stats, ws, as_stream(stream));
   });
 }
 
@@ -258,8 +260,7 @@ int gpcx_lut_gen_device(const uint16_t* img, uint64_t n, int mode, uint16_t* lut
     need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
     const cudaStream_t s = as_stream(stream);
     if (mode == GPCX_LUT_EQUALIZE) {
-      gpcx::lut::launch_hist(img, n, gpcx::lut::ws_hist(ws), ws, s);
-      gpcx::lut::launch_from_hist(gpcx::lut::ws_hist(ws), mode, lut, stats, s);
+      gpcx::lut::launch_hist_lut(img, n, mode, lut, stats, ws, s);
     } else if (mode == GPCX_LUT_STRETCH) {
       gpcx::lut::launch_minmax(img, n, stats, ws, s);
       gpcx::lut::launch_from_minmax(stats, lut, s);

@@ -166,8 +166,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     if (flag != Flag::LutApply) {
       if (G == 1) {
         if (equalize) {
-          lut::launch_hist(dimg, bn, s.d_hist(), s.lut_ws.ptr, s.stream);
-          lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.stream);
+          lut::launch_hist_lut(dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr, s.stream);
         } else {
           lut::launch_minmax(dimg, bn, s.d_stats(), s.lut_ws.ptr, s.stream);
           lut::launch_from_minmax(s.d_stats(), s.d_lut(), s.stream);
@@ -175,7 +174,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       } else if (equalize) {
         GPCX_CUDA(cudaMemcpyAsync(s.d_hist(), global_hist.data(), 65536 * 4,
                                   cudaMemcpyHostToDevice, s.stream));
-        lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.stream);
+        lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr, s.stream);
       } else {
         GPCX_CUDA(cudaMemcpyAsync(s.d_stats(), &global_mm, sizeof(global_mm),
                                   cudaMemcpyHostToDevice, s.stream));

@@ -32,8 +32,14 @@ int parts_for(std::uint64_t n, int num_sms);
 
 void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
                  void* ws, cudaStream_t stream);
+// LUT + stats from a merged histogram (cooperative build kernel; `ws` is a
+// LUT workspace, used for the per-CTA scan triples).
 void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
-                      gpcx_lut_stats* stats, cudaStream_t stream);
+                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+// Single-device LUT_GEN equalize/stretch-from-histogram: hist_kernel + the
+// fused merge/build kernel (the histogram lands in ws_hist(ws)).
+void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
+                     gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 void launch_minmax(const std::uint16_t* img, std::uint64_t n,
                    gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 void launch_from_minmax(const gpcx_lut_stats* stats, std::uint16_t* lut,

@@ -15,6 +15,7 @@
 //   from_minmax     stretch LUT.
 //   apply_kernel    persistent, LUT staged in 128 KiB smem, 128-bit
 //                   loads/stores, 8 gathers per vector.   4 B/px.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,18 +41,21 @@ int device_sm_count() {
 
 namespace lut {
 
+namespace cg = cooperative_groups;
+
 namespace {
 
 constexpr int kThreads = 1024;
 constexpr std::uint64_t kOverflowOff = 0;
 constexpr std::uint64_t kHistOff = 256 * 1024;
 constexpr std::uint64_t kMinMaxOff = 512 * 1024;
+constexpr std::uint64_t kBlocksOff = kMinMaxOff + 4 * 1024;  // build_kernel's 128 triples
 constexpr std::uint64_t kPartsOff = kMinMaxOff + 8 * 1024;
 constexpr int kSmemHist = kWords * 4;  // 128 KiB
 constexpr int kSmemLut = kBins * 2;    // 128 KiB
 constexpr int kUnroll = 4;
 
-static_assert(kMaxParts * 8 <= 8 * 1024, "min/max slot area");
+static_assert(kMaxParts * 8 <= 4 * 1024, "min/max slot area");
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
@@ -74,13 +78,13 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 // a low-half carry into the high half, the spurious +1) into the global
 // overflow counters; the merge adds them back mod 2^32.  Exact for any
 // count < 2^32 and independent of the interleaving.
-__device__ __forceinline__ void count_one(std::uint32_t* bins,
-                                          std::uint32_t* overflow,
-                                          std::uint32_t v) {
-  const std::uint32_t hi_bin = v & 1u;
-  const std::uint32_t inc = hi_bin ? 0x10000u : 1u;
-  const std::uint32_t mask = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
-  const std::uint32_t old = atomicAdd(&bins[v >> 1], inc);
+__device__ __forceinline__ void count_one(uint32_t* bins,
+                                          uint32_t* overflow,
+                                          uint32_t v) {
+  const uint32_t hi_bin = v & 1u;
+  const uint32_t inc = hi_bin ? 0x10000u : 1u;
+  const uint32_t mask = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+  const uint32_t old = atomicAdd(&bins[v >> 1], inc);
   if ((old & mask) == mask) {
     atomicAdd(&overflow[v], 65536u);
     if (!hi_bin) {
@@ -92,8 +96,8 @@ __device__ __forceinline__ void count_one(std::uint32_t* bins,
   }
 }
 
-__device__ __forceinline__ void count_vec(std::uint32_t* bins,
-                                          std::uint32_t* overflow, uint4 q) {
+__device__ __forceinline__ void count_vec(uint32_t* bins,
+                                          uint32_t* overflow, uint4 q) {
   count_one(bins, overflow, q.x & 0xFFFFu);
   count_one(bins, overflow, q.x >> 16);
   count_one(bins, overflow, q.y & 0xFFFFu);
@@ -115,10 +119,10 @@ __device__ __host__ __forceinline__ std::uint64_t head_len(const void* p,
 
 __global__ void __launch_bounds__(kThreads, 1)
     hist_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
-                std::uint32_t* __restrict__ parts,
-                std::uint32_t* __restrict__ overflow) {
+                uint32_t* __restrict__ parts,
+                uint32_t* __restrict__ overflow) {
   extern __shared__ uint4 smem_u4[];
-  std::uint32_t* bins = reinterpret_cast<std::uint32_t*>(smem_u4);
+  uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
   for (int i = threadIdx.x; i < kWords / 4; i += kThreads)
     smem_u4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
@@ -138,12 +142,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint4* body = reinterpret_cast<const uint4*>(img + head);
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
   std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
-  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
-    uint4 q[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(body + i + u * stride);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) count_vec(bins, overflow, q[u]);
+  // Two-vector software pipeline: the next stage's loads are in flight while
+  // this stage's 16 samples are counted (tools/hist_bench.cu: 5% faster than
+  // load-then-count; the smem atomic rate is the remaining bound).
+  {
+    uint4 q[2], nq[2];
+    bool have = i + stride < nvec;
+    if (have) {
+      q[0] = ld_stream(body + i);
+      q[1] = ld_stream(body + i + stride);
+    }
+    while (have) {
+      const std::uint64_t nx = i + 2 * stride;
+      const bool nhave = nx + stride < nvec;
+      if (nhave) {
+        nq[0] = ld_stream(body + nx);
+        nq[1] = ld_stream(body + nx + stride);
+      }
+      count_vec(bins, overflow, q[0]);
+      count_vec(bins, overflow, q[1]);
+      q[0] = nq[0];
+      q[1] = nq[1];
+      i = nx;
+      have = nhave;
+    }
   }
   for (; i < nvec; i += stride) count_vec(bins, overflow, ld_stream(body + i));
   __syncthreads();
@@ -155,15 +177,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // hist[2w], hist[2w+1] = column sums of the packed partials + overflow;
 // leaves the overflow counters zeroed for the next call.
 __global__ void __launch_bounds__(256)
-    merge_kernel(const std::uint32_t* __restrict__ parts, int nparts,
-                 std::uint32_t* __restrict__ overflow,
-                 std::uint32_t* __restrict__ hist) {
+    merge_kernel(const uint32_t* __restrict__ parts, int nparts,
+                 uint32_t* __restrict__ overflow,
+                 uint32_t* __restrict__ hist) {
   const int w = blockIdx.x * 256 + threadIdx.x;
   if (w >= kWords) return;
-  std::uint32_t lo = 0, hi = 0;
+  uint32_t lo = 0, hi = 0;
   int p = 0;
   for (; p + 4 <= nparts; p += 4) {
-    std::uint32_t x[4];
+    uint32_t x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = parts[static_cast<std::uint64_t>(p + u) * kWords + w];
 #pragma unroll
@@ -173,7 +195,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   for (; p < nparts; ++p) {
-    const std::uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
+    const uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
     lo += x & 0xFFFFu;
     hi += x >> 16;
   }
@@ -196,25 +218,25 @@ __device__ __forceinline__ std::uint64_t udiv_exact(std::uint64_t num, std::uint
 }
 
 // LUT entry for bin v given the statistics (SURVEY §8a' formulas).
-__device__ __forceinline__ std::uint32_t equalize_entry(std::uint32_t v,
+__device__ __forceinline__ uint32_t equalize_entry(uint32_t v,
                                                         std::uint64_t cdf,
                                                         std::uint64_t cdf_min,
                                                         std::uint64_t d, double inv_d,
-                                                        std::uint32_t lo) {
+                                                        uint32_t lo) {
   if (d == 0) return v;
   if (v < lo) return 0;
-  return static_cast<std::uint32_t>(udiv_exact((cdf - cdf_min) * 65535u + d / 2, d, inv_d));
+  return static_cast<uint32_t>(udiv_exact((cdf - cdf_min) * 65535u + d / 2, d, inv_d));
 }
 
-__device__ __forceinline__ std::uint32_t stretch_entry(std::uint64_t v,
+__device__ __forceinline__ uint32_t stretch_entry(std::uint64_t v,
                                                        std::uint64_t n,
                                                        std::uint64_t lo,
                                                        std::uint64_t hi) {
   const std::uint64_t span = hi - lo;
-  if (n == 0 || span == 0) return static_cast<std::uint32_t>(v);
+  if (n == 0 || span == 0) return static_cast<uint32_t>(v);
   if (v <= lo) return 0;
   if (v >= hi) return 65535;
-  return static_cast<std::uint32_t>(
+  return static_cast<uint32_t>(
       udiv_exact((v - lo) * 65535u + span / 2, span, 1.0 / static_cast<double>(span)));
 }
 
@@ -225,28 +247,28 @@ __device__ __forceinline__ std::uint32_t stretch_entry(std::uint64_t v,
 // warp-shuffle inclusive scan of each 32-bin row -> cdf -> LUT entries,
 // written as coalesced 64-byte rows.
 __global__ void __launch_bounds__(1024, 1)
-    from_hist_kernel(const std::uint32_t* __restrict__ hist, int mode,
+    from_hist_kernel(const uint32_t* __restrict__ hist, int mode,
                      std::uint16_t* __restrict__ lut,
                      gpcx_lut_stats* __restrict__ stats) {
   constexpr int kRows = kBins / 1024;  // 64 rows of 32 bins per warp
-  __shared__ std::uint32_t s_tot[32], s_lo[32], s_hi[32];
+  __shared__ uint32_t s_tot[32], s_lo[32], s_hi[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::uint32_t base = static_cast<std::uint32_t>(warp) * (kRows * 32);
-  const std::uint32_t* hw = hist + base + lane;
+  const uint32_t base = static_cast<uint32_t>(warp) * (kRows * 32);
+  const uint32_t* hw = hist + base + lane;
 
-  std::uint32_t acc = 0, first = 0xFFFFFFFFu, last = 0;
+  uint32_t acc = 0, first = 0xFFFFFFFFu, last = 0;
 #pragma unroll 8
   for (int r = 0; r < kRows; ++r) {
-    const std::uint32_t x = __ldg(hw + r * 32);
+    const uint32_t x = __ldg(hw + r * 32);
     acc += x;
     if (x != 0) {
       first = min(first, base + r * 32 + lane);
       last = base + r * 32 + lane;
     }
   }
-  const std::uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, acc);
-  const std::uint32_t wlo = __reduce_min_sync(0xFFFFFFFFu, first);
-  const std::uint32_t whi = __reduce_max_sync(0xFFFFFFFFu, last);
+  const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, acc);
+  const uint32_t wlo = __reduce_min_sync(0xFFFFFFFFu, first);
+  const uint32_t whi = __reduce_max_sync(0xFFFFFFFFu, last);
   if (lane == 0) {
     s_tot[warp] = wtot;
     s_lo[warp] = wlo;
@@ -254,17 +276,17 @@ __global__ void __launch_bounds__(1024, 1)
   }
   __syncthreads();
   // every warp redoes the 32-entry reductions (cheaper than another barrier)
-  const std::uint32_t t = s_tot[lane];
-  std::uint32_t incl = t;
+  const uint32_t t = s_tot[lane];
+  uint32_t incl = t;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
     if (lane >= d) incl += y;
   }
-  const std::uint32_t n32 = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  const std::uint32_t offset = __shfl_sync(0xFFFFFFFFu, incl - t, warp);
-  const std::uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, s_lo[lane]);
-  const std::uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, s_hi[lane]);
+  const uint32_t n32 = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  const uint32_t offset = __shfl_sync(0xFFFFFFFFu, incl - t, warp);
+  const uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, s_lo[lane]);
+  const uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, s_hi[lane]);
   const std::uint64_t n = n32;
 
   std::uint16_t* lw = lut + base + lane;
@@ -283,20 +305,20 @@ __global__ void __launch_bounds__(1024, 1)
   std::uint64_t carry = offset;
 #pragma unroll 4
   for (int r = 0; r < kRows; ++r) {
-    const std::uint32_t v = base + r * 32 + lane;
-    std::uint32_t x = __ldg(hw + r * 32);
-    std::uint32_t inc = x;
+    const uint32_t v = base + r * 32 + lane;
+    uint32_t x = __ldg(hw + r * 32);
+    uint32_t inc = x;
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, dd);
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, dd);
       if (lane >= dd) inc += y;
     }
-    std::uint32_t e;
+    uint32_t e;
     if (mode == GPCX_LUT_STRETCH) {
       if (span == 0) e = v;
       else if (v <= lo) e = 0;
       else if (v >= hi) e = 65535;
-      else e = static_cast<std::uint32_t>(udiv_exact((v - lo) * 65535ull + span / 2, span, inv_span));
+      else e = static_cast<uint32_t>(udiv_exact((v - lo) * 65535ull + span / 2, span, inv_span));
     } else {
       e = equalize_entry(v, carry + inc, cdf_min, d, inv_d, lo);
     }
@@ -305,8 +327,123 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-__device__ __forceinline__ void minmax_vec(uint4 q, std::uint32_t& mn2,
-                                           std::uint32_t& mx2) {
+// Fused histogram merge + LUT build, one cooperative grid of 128 CTAs x 256
+// threads (every CTA resident): thread t of CTA b owns bins 2w, 2w+1 with
+// w = 256b + t.
+//   phase 1  merge the per-CTA packed partials (+ overflow, which it zeroes)
+//            into hist[] -- or take hist[] as given (multi-GPU: all-reduced)
+//            -- and publish per-CTA totals / first / last non-empty bins;
+//   grid.sync
+//   phase 2  every CTA derives n, lo, hi and its cdf offset from the 128
+//            published triples, scans its 512 bins and writes its LUT slice.
+// Replaces merge_kernel + the single-CTA from_hist_kernel on the hot path.
+constexpr int kBuildCtas = kWords / 256;  // 128
+
+__global__ void __launch_bounds__(256)
+    build_kernel(const uint32_t* __restrict__ parts, int nparts,
+                 uint32_t* __restrict__ overflow, uint32_t* __restrict__ hist,
+                 int merge, int mode, uint3* __restrict__ blocks,
+                 std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats) {
+  __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int w = blockIdx.x * 256 + t;
+  uint32_t c0, c1;
+  if (merge) {
+    uint32_t lo = 0, hi = 0;
+    int p = 0;
+    for (; p + 4 <= nparts; p += 4) {
+      uint32_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = parts[static_cast<std::uint64_t>(p + u) * kWords + w];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        lo += x[u] & 0xFFFFu;
+        hi += x[u] >> 16;
+      }
+    }
+    for (; p < nparts; ++p) {
+      const uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
+      lo += x & 0xFFFFu;
+      hi += x >> 16;
+    }
+    const uint2 ov = reinterpret_cast<const uint2*>(overflow)[w];
+    reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
+    c0 = lo + ov.x;
+    c1 = hi + ov.y;
+    reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
+  } else {
+    const uint2 h = reinterpret_cast<const uint2*>(hist)[w];
+    c0 = h.x;
+    c1 = h.y;
+  }
+  // CTA totals: warp inclusive scan of (c0 + c1), then across 8 warps.
+  const uint32_t pair = c0 + c1;
+  uint32_t inc = pair;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  const uint32_t first = c0 ? 2u * w : (c1 ? 2u * w + 1 : 0xFFFFFFFFu);
+  const uint32_t last = c1 ? 2u * w + 1 : (c0 ? 2u * w : 0u);
+  const uint32_t wfirst = __reduce_min_sync(0xFFFFFFFFu, first);
+  const uint32_t wlast = __reduce_max_sync(0xFFFFFFFFu, last);
+  if (lane == 31) s_wsum[warp] = inc;
+  if (lane == 0) {
+    s_wfirst[warp] = wfirst;
+    s_wlast[warp] = wlast;
+  }
+  __syncthreads();
+  uint32_t warp_off = 0, cta_sum = 0, cta_first = 0xFFFFFFFFu, cta_last = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < warp) warp_off += s_wsum[i];
+    cta_sum += s_wsum[i];
+    cta_first = min(cta_first, s_wfirst[i]);
+    cta_last = max(cta_last, s_wlast[i]);
+  }
+  if (t == 0) blocks[blockIdx.x] = make_uint3(cta_sum, cta_first, cta_last);
+  cg::this_grid().sync();
+
+  // Phase 2: global n / lo / hi and this CTA's offset from the 128 triples.
+  uint32_t n32 = 0, off = 0, lo = 0xFFFFFFFFu, hi = 0;
+  for (int b = lane; b < kBuildCtas; b += 32) {
+    const uint3 q = blocks[b];
+    n32 += q.x;
+    if (b < static_cast<int>(blockIdx.x)) off += q.x;
+    lo = min(lo, q.y);
+    if (q.x != 0) hi = max(hi, q.z);
+  }
+  n32 = __reduce_add_sync(0xFFFFFFFFu, n32);
+  off = __reduce_add_sync(0xFFFFFFFFu, off);
+  lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+  hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+  const uint32_t v0 = 2u * w;
+  uint32_t e0, e1;
+  if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
+    e0 = v0;
+    e1 = v0 + 1;
+    if (w == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
+  } else {
+    const std::uint64_t n = n32;
+    const std::uint64_t cdf_min = hist[lo];
+    if (w == 0) *stats = gpcx_lut_stats{n, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
+    if (mode == GPCX_LUT_STRETCH) {
+      e0 = stretch_entry(v0, n, lo, hi);
+      e1 = stretch_entry(v0 + 1, n, lo, hi);
+    } else {
+      const std::uint64_t d = n - cdf_min;
+      const double inv_d = d != 0 ? 1.0 / static_cast<double>(d) : 0.0;
+      const std::uint64_t cdf1 = static_cast<std::uint64_t>(off) + warp_off + inc;  // through v0+1
+      e0 = equalize_entry(v0, cdf1 - c1, cdf_min, d, inv_d, lo);
+      e1 = equalize_entry(v0 + 1, cdf1, cdf_min, d, inv_d, lo);
+    }
+  }
+  reinterpret_cast<uint32_t*>(lut)[w] = e0 | (e1 << 16);
+}
+
+__device__ __forceinline__ void minmax_vec(uint4 q, uint32_t& mn2,
+                                           uint32_t& mx2) {
   mn2 = __vminu2(mn2, __vminu2(__vminu2(q.x, q.y), __vminu2(q.z, q.w)));
   mx2 = __vmaxu2(mx2, __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w)));
 }
@@ -316,20 +453,20 @@ __device__ __forceinline__ void minmax_vec(uint4 q, std::uint32_t& mn2,
 __global__ void __launch_bounds__(kThreads)
     minmax_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
                   uint2* __restrict__ slots) {
-  __shared__ std::uint32_t smn[32], smx[32];
-  std::uint32_t mn2 = 0xFFFFFFFFu, mx2 = 0;
+  __shared__ uint32_t smn[32], smx[32];
+  uint32_t mn2 = 0xFFFFFFFFu, mx2 = 0;
   const std::uint64_t head = head_len(img, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t tail0 = head + (nvec << 3);
   const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
   if (tid < head) {
-    const std::uint32_t v = img[tid];
+    const uint32_t v = img[tid];
     mn2 = __vminu2(mn2, v | (v << 16));
     mx2 = __vmaxu2(mx2, v | (v << 16));
   }
   if (tid < n - tail0) {
-    const std::uint32_t v = img[tail0 + tid];
+    const uint32_t v = img[tail0 + tid];
     mn2 = __vminu2(mn2, v | (v << 16));
     mx2 = __vmaxu2(mx2, v | (v << 16));
   }
@@ -344,8 +481,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   for (; i < nvec; i += stride) minmax_vec(ld_stream(body + i), mn2, mx2);
 
-  std::uint32_t mn = min(mn2 & 0xFFFFu, mn2 >> 16);
-  std::uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
+  uint32_t mn = min(mn2 & 0xFFFFu, mn2 >> 16);
+  uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
   mn = __reduce_min_sync(0xFFFFFFFFu, mn);
   mx = __reduce_max_sync(0xFFFFFFFFu, mx);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -364,8 +501,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(1024)
     minmax_reduce_kernel(const uint2* __restrict__ slots, int nslots,
                          std::uint64_t n, gpcx_lut_stats* __restrict__ stats) {
-  __shared__ std::uint32_t smn[32], smx[32];
-  std::uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  __shared__ uint32_t smn[32], smx[32];
+  uint32_t mn = 0xFFFFFFFFu, mx = 0;
   for (int i = threadIdx.x; i < nslots; i += 1024) {
     const uint2 s = slots[i];
     mn = min(mn, s.x);
@@ -398,10 +535,10 @@ __global__ void __launch_bounds__(1024)
   const int b0 = threadIdx.x * 64;
   uint4* dst = reinterpret_cast<uint4*>(lut + b0);
   for (int j = 0; j < 8; ++j) {
-    std::uint32_t w[4];
+    uint32_t w[4];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const std::uint32_t r = stretch_entry(b0 + 8 * j + u, n, lo, hi);
+      const uint32_t r = stretch_entry(b0 + 8 * j + u, n, lo, hi);
       if (u & 1) w[u >> 1] |= r << 16;
       else w[u >> 1] = r;
     }
@@ -411,10 +548,10 @@ __global__ void __launch_bounds__(1024)
 
 __device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
   uint4 r;
-  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.x >> 16]) << 16);
-  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.y >> 16]) << 16);
-  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.z >> 16]) << 16);
-  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<std::uint32_t>(s_lut[q.w >> 16]) << 16);
+  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.x >> 16]) << 16);
+  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.y >> 16]) << 16);
+  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.z >> 16]) << 16);
+  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.w >> 16]) << 16);
   return r;
 }
 
@@ -447,13 +584,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint4* src = reinterpret_cast<const uint4*>(in + head);
   uint4* dst = reinterpret_cast<uint4*>(out + head);
+  // Software pipeline, two vectors per stage: the loads of stage g+1 are in
+  // flight while stage g is looked up and stored, so the smem gathers never
+  // leave the memory system without requests (tools/apply_bench.cu: 6.48
+  // TB/s, = cudaMemcpy D2D, vs 5.6-5.9 TB/s for the load-then-use loop).
+  constexpr int kU = 2;
   std::uint64_t i = tid;
-  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
-    uint4 q[kUnroll];
+  uint4 q[kU], nq[kU];
+  bool have = i + (kU - 1) * stride < nvec;
+  if (have) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(src + i + u * stride);
+    for (int u = 0; u < kU; ++u) q[u] = ld_stream(src + i + u * stride);
+  }
+  while (have) {
+    const std::uint64_t nx = i + kU * stride;
+    const bool nhave = nx + (kU - 1) * stride < nvec;
+    if (nhave) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
+      for (int u = 0; u < kU; ++u) nq[u] = ld_stream(src + nx + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
+#pragma unroll
+    for (int u = 0; u < kU; ++u) q[u] = nq[u];
+    i = nx;
+    have = nhave;
   }
   for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
 }
@@ -473,8 +628,8 @@ void set_attrs_once() {
 
 }  // namespace
 
-std::uint32_t* ws_hist(void* ws) {
-  return reinterpret_cast<std::uint32_t*>(static_cast<unsigned char*>(ws) + kHistOff);
+uint32_t* ws_hist(void* ws) {
+  return reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ws) + kHistOff);
 }
 
 std::uint64_t workspace_bytes() {
@@ -489,12 +644,12 @@ int parts_for(std::uint64_t n, int num_sms) {
   return std::max(1, std::min(p, kMaxParts));
 }
 
-void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
+void launch_hist(const std::uint16_t* img, std::uint64_t n, uint32_t* hist,
                  void* ws, cudaStream_t stream) {
   set_attrs_once();
   auto* base = static_cast<unsigned char*>(ws);
-  auto* overflow = reinterpret_cast<std::uint32_t*>(base + kOverflowOff);
-  auto* parts = reinterpret_cast<std::uint32_t*>(base + kPartsOff);
+  auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
+  auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
   const int p = parts_for(n, device_sm_count());
   hist_kernel<<<p, kThreads, kSmemHist, stream>>>(img, n, parts, overflow);
   GPCX_LAUNCH_CHECK();
@@ -502,10 +657,34 @@ void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
   GPCX_LAUNCH_CHECK();
 }
 
-void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
-                      gpcx_lut_stats* stats, cudaStream_t stream) {
-  from_hist_kernel<<<1, 1024, 0, stream>>>(hist, mode, lut, stats);
+namespace {
+void launch_build(const uint32_t* parts, int nparts, uint32_t* overflow,
+                  uint32_t* hist, int merge, int mode, void* ws, std::uint16_t* lut,
+                  gpcx_lut_stats* stats, cudaStream_t stream) {
+  auto* blocks = reinterpret_cast<uint3*>(static_cast<unsigned char*>(ws) + kBlocksOff);
+  void* args[] = {&parts, &nparts, &overflow, &hist, &merge, &mode, &blocks, &lut, &stats};
+  GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(build_kernel),
+                                        dim3(kBuildCtas), dim3(256), args, 0, stream));
+}
+}  // namespace
+
+void launch_from_hist(const uint32_t* hist, int mode, std::uint16_t* lut,
+                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  launch_build(nullptr, 0, nullptr, const_cast<uint32_t*>(hist), 0, mode, ws, lut, stats,
+               stream);
+}
+
+void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
+                     gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  set_attrs_once();
+  auto* base = static_cast<unsigned char*>(ws);
+  auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
+  auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
+  auto* hist = reinterpret_cast<uint32_t*>(base + kHistOff);
+  const int p = parts_for(n, device_sm_count());
+  hist_kernel<<<p, kThreads, kSmemHist, stream>>>(img, n, parts, overflow);
   GPCX_LAUNCH_CHECK();
+  launch_build(parts, p, overflow, hist, 1, mode, ws, lut, stats, stream);
 }
 
 void launch_minmax(const std::uint16_t* img, std::uint64_t n,

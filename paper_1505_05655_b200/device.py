@@ -49,8 +49,9 @@ def lut_hist(img, hist, ws, stream=None):
     check(lib.gpcx_lut_hist_device(_p(img), img.numel(), _p(hist), _p(ws), ws.numel(), _s(stream)))
 
 
-def lut_from_hist(hist, mode, lut, stats, stream=None):
-    check(lib.gpcx_lut_from_hist_device(_p(hist), mode, _p(lut), _p(stats), _s(stream)))
+def lut_from_hist(hist, mode, lut, stats, ws, stream=None):
+    check(lib.gpcx_lut_from_hist_device(_p(hist), mode, _p(lut), _p(stats), _p(ws), ws.numel(),
+                                        _s(stream)))
 
 
 def lut_minmax(img, stats, ws, stream=None):

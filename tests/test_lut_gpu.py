@@ -93,7 +93,7 @@ def test_from_hist_and_minmax_paths_agree(gpu, mode):
     ws = D.lut_workspace(img.numel())
     D.lut_hist(img, hist, ws)
     lut_a, st_a = D.new_lut(), D.new_stats()
-    D.lut_from_hist(hist, mode, lut_a, st_a)
+    D.lut_from_hist(hist, mode, lut_a, st_a, ws)
     lut_b, st_b = D.new_lut(), D.new_stats()
     D.lut_gen(img, mode, lut_b, st_b, ws)
     assert np.array_equal(u16(lut_a), u16(lut_b))

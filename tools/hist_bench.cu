@@ -34,7 +34,7 @@ __device__ __forceinline__ uint4 ldnc(const uint4* p) {
 // MODE 2: loads only (xor sink)
 // MODE 3: red via inline PTX red.shared.add.u32
 // MODE 4: pair-merge: if both halves of a u32 land in the same word, one atom
-template <int MODE, int THREADS>
+template <int MODE, int THREADS, bool PIPE = false>
 __global__ void __launch_bounds__(THREADS, 1) hist(const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* ovf) {
   extern __shared__ uint4 sm[];
   uint32_t* bins = (uint32_t*)sm;
@@ -72,6 +72,20 @@ __global__ void __launch_bounds__(THREADS, 1) hist(const uint16_t* img, uint64_t
     }
   };
   uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+  if (PIPE) {  // loads of stage g+1 in flight while stage g is counted
+    uint4 q[2], nq[2];
+    bool have = i + stride < nvec;
+    if (have) { q[0] = ldnc(body + i); q[1] = ldnc(body + i + stride); }
+    while (have) {
+      const uint64_t nx = i + 2 * stride;
+      const bool nhave = nx + stride < nvec;
+      if (nhave) { nq[0] = ldnc(body + nx); nq[1] = ldnc(body + nx + stride); }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) { word(q[u].x); word(q[u].y); word(q[u].z); word(q[u].w); }
+      q[0] = nq[0]; q[1] = nq[1];
+      i = nx; have = nhave;
+    }
+  }
   for (; i + 3 * stride < nvec; i += 4 * stride) {
     uint4 q[4];
 #pragma unroll
@@ -86,15 +100,15 @@ __global__ void __launch_bounds__(THREADS, 1) hist(const uint16_t* img, uint64_t
   for (int j = threadIdx.x; j < 8192; j += THREADS) dst[j] = sm[j];
 }
 
-template <int MODE, int THREADS>
+template <int MODE, int THREADS, bool PIPE = false>
 int run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* ovf, int sms) {
-  CK(cudaFuncSetAttribute(hist<MODE, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
+  CK(cudaFuncSetAttribute(hist<MODE, THREADS, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072));
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   std::vector<float> ts;
   for (int r = 0; r < 8; ++r) {
     cudaEventRecord(a);
-    hist<MODE, THREADS><<<sms, THREADS, 131072>>>(img, n, parts, ovf);
+    hist<MODE, THREADS, PIPE><<<sms, THREADS, 131072>>>(img, n, parts, ovf);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms; cudaEventElapsedTime(&ms, a, b); ts.push_back(ms);
@@ -120,6 +134,9 @@ int main() {
     run<2, 1024>("loads only 1024", img, n, parts, ovf, sms);
     run<3, 1024>("red.shared 1024", img, n, parts, ovf, sms);
     run<4, 1024>("pair-merge 1024", img, n, parts, ovf, sms);
+    run<0, 1024, true>("atom+check 1024 pipelined", img, n, parts, ovf, sms);
+    run<1, 1024, true>("atom noret 1024 pipelined", img, n, parts, ovf, sms);
+    run<0, 768, true>("atom+check 768 pipelined", img, n, parts, ovf, sms);
   }
   return 0;
 }

@@ -31,16 +31,19 @@ def main():
     for kind, name in ((0, "ramp12"), (1, "uniform16")):
         img = D.synth_image(kind, 0x5EED, args.rows, args.cols)
         D.lut_hist(img, hist, ws)
-        D.lut_from_hist(hist, 0, lut, stats)
+        D.lut_from_hist(hist, 0, lut, stats, ws)
         ops = {
             "hist+merge": lambda: D.lut_hist(img, hist, ws),
-            "from_hist": lambda: D.lut_from_hist(hist, 0, lut, stats),
+            "from_hist": lambda: D.lut_from_hist(hist, 0, lut, stats, ws),
+            "gen(hist+fused build)": lambda: D.lut_gen(img, 0, lut, stats, ws),
+            "correct(gen+apply)": lambda: D.lut_correct(img, out, 0, lut, stats, ws),
             "minmax": lambda: D.lut_minmax(img, stats, ws),
             "apply": lambda: D.lut_apply(lut, img, out),
             "copy(torch)": lambda: out.copy_(img),
         }
         bytes_per = {"hist+merge": 2 * n, "from_hist": 0, "minmax": 2 * n, "apply": 4 * n,
-                     "copy(torch)": 4 * n}
+                     "copy(torch)": 4 * n, "gen(hist+fused build)": 2 * n,
+                     "correct(gen+apply)": 6 * n}
         for op, fn in ops.items():
             ts = []
             for _ in range(args.reps + 2):
