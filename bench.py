@@ -226,36 +226,52 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
             "stats": st, "clocks": clk.summary()}
 
 
-def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int) -> dict:
+def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int = 1) -> dict:
     """Rank 0, all N GPUs bound in-process: gpcx_lut_host with pinned host
-    buffers (H2D + kernels + D2H per step)."""
+    buffers (H2D + kernels + D2H per step).  `inflight` requests are issued
+    concurrently from that many host threads (a server with several requests
+    queued): one request's H2D then overlaps another's D2H on the
+    full-duplex PCIe link.  value = scenes corrected per second x pixels."""
     import ctypes as C
+    import threading as th
     import torch
     import paper_1505_05655_b200 as G
     from paper_1505_05655_b200 import device as D
     G.init(list(range(n_gpus)))
     n = ROWS * COLS
-    p_in = G.lib.gpcx_pinned_alloc(n * 2)
-    p_out = G.lib.gpcx_pinned_alloc(n * 2)
+    bufs = [(G.lib.gpcx_pinned_alloc(n * 2), G.lib.gpcx_pinned_alloc(n * 2)) for _ in range(inflight)]
     try:
-        host_in = np.ctypeslib.as_array((C.c_uint16 * n).from_address(p_in))
-        host_in[:] = D.synth_image(0, SEED, ROWS, COLS).cpu().numpy().view(np.uint16)
+        scene = D.synth_image(0, SEED, ROWS, COLS).cpu().numpy().view(np.uint16)
+        for p_in, _ in bufs:
+            np.ctypeslib.as_array((C.c_uint16 * n).from_address(p_in))[:] = scene
+        del scene
         torch.cuda.empty_cache()
-        st = G.LutStats()
-        times = []
-        for i in range(warmup + steps):
-            t = time.perf_counter()
+
+        def one(p_in, p_out):
+            st = G.LutStats()
             G.check(G.lib.gpcx_lut_host(2, mode, ROWS, COLS, C.c_void_p(p_in), None,
                                         C.c_void_p(p_out), None, C.byref(st)))
-            if i >= warmup:
-                times.append(time.perf_counter() - t)
+
+        def worker(k, p_in, p_out, count):
+            for _ in range(count):
+                one(p_in, p_out)
+
+        for _ in range(warmup):
+            one(*bufs[0])
+        per = max(1, steps // inflight)
+        t = time.perf_counter()
+        ts = [th.Thread(target=worker, args=(k, *bufs[k], per)) for k in range(inflight)]
+        [x.start() for x in ts]
+        [x.join() for x in ts]
+        wall = time.perf_counter() - t
     finally:
-        G.lib.gpcx_pinned_free(p_in)
-        G.lib.gpcx_pinned_free(p_out)
+        for p_in, p_out in bufs:
+            G.lib.gpcx_pinned_free(p_in)
+            G.lib.gpcx_pinned_free(p_out)
         G.init([0])
-    tot = sum(times)
-    return {"value": n * steps / tot / 1e9, "ms_per_step": 1e3 * tot / steps,
-            "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": n * 2}
+    done = per * inflight
+    return {"value": n * done / wall / 1e9, "ms_per_step": 1e3 * wall / done,
+            "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": n * 2, "inflight": inflight}
 
 
 MM4 = 32768  # config C4
@@ -515,12 +531,18 @@ def run_b200(args) -> None:
                        "parallelism": f"row-band x{d.n}, NCCL all-reduce of the 65536-bin histogram",
                        "l2": "inputs larger than L2 (2 GiB scene)"},
             "roofline": roof, "gpu_launches": 4 * args.steps, "clocks": lut["clocks"]}
-    e2e = lut_e2e_leg(d.n, max(2, min(args.steps, 5)), 1, mode)
-    line["e2e"] = {"value": round(e2e["value"], 3), "unit": "Gpixel/s",
-                   "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
-                   "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
-                   "ms_per_step": round(e2e["ms_per_step"], 2),
-                   "path": "gpcx_lut_host (C ABI), pinned host buffers, all N GPUs in-process"}
+    e2e_steps = max(4, min(args.steps, 8))
+    e2e1 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=1)
+    e2e2 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=2)
+    best = e2e2 if e2e2["value"] > e2e1["value"] else e2e1
+    line["e2e"] = {"value": round(best["value"], 3), "unit": "Gpixel/s",
+                   "h2d_bytes_per_step": best["h2d_bytes_per_step"],
+                   "d2h_bytes_per_step": best["d2h_bytes_per_step"],
+                   "ms_per_step": round(best["ms_per_step"], 2), "inflight": best["inflight"],
+                   "single_request": {"value": round(e2e1["value"], 3),
+                                      "ms_per_step": round(e2e1["ms_per_step"], 2)},
+                   "path": "gpcx_lut_host (C ABI), pinned host buffers, all N GPUs in-process; "
+                           "each step = one full C3 scene in (2 GiB H2D) and out (2 GiB D2H)"}
     if d.n == 1:
         line["cpu_baseline"] = cpu_lut(mode)
     if c4 is not None:
