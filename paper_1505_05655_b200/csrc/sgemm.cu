@@ -7,12 +7,16 @@
 // plain fp32 FFMA accumulation in a fixed, K-ascending order per output, so
 // results are deterministic and identical for any block-row sharding.
 //
-// Tiling: 128x128 CTA tile, BK = 16, 256 threads each owning an 8x8 block
-// (2x2 quads of 4x4 so the 128-bit smem reads stay conflict-free), A staged
-// transposed, double-buffered smem with register prefetch of the next tile.
+// Tiling: 128x128 CTA tile, BK = 8 or 16, 256 threads each owning an 8x8
+// block (2x2 quads of 4x4 so the 128-bit smem reads stay conflict-free), A
+// staged transposed, double-buffered smem with register prefetch of the
+// next tile.  Variant <BK, min CTAs/SM> is picked per launch
+// (GPCX_SGEMM=16x1|8x2|16x2 overrides, for A/B measurement).
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "cuda_util.hpp"
 #include "kernels.hpp"
@@ -21,13 +25,14 @@ namespace gpcx::gemm {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256;
+constexpr int BM = 128, BN = 128, THREADS = 256;
 
-template <bool kChecked>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int BK, int MINB, bool kChecked>
+__global__ void __launch_bounds__(THREADS, MINB)
     sgemm_kernel(int m, int n, int k, const float* __restrict__ A,
                  std::uint64_t lda, const float* __restrict__ B,
                  std::uint64_t ldb, float* __restrict__ C, std::uint64_t ldc) {
+  constexpr int kLoads = BK / 8;  // float4 of A and of B per thread per tile
   __shared__ __align__(16) float As[2][BK][BM];
   __shared__ __align__(16) float Bs[2][BK][BN];
 
@@ -35,23 +40,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
 
-  // Global-load coordinates: two float4 of A and two of B per thread.
-  int a_row[2], a_k4[2], b_k[2], b_c4[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int f = tid + THREADS * i;
-    a_row[i] = f & (BM - 1);
-    a_k4[i] = f >> 7;  // 0..3
-    b_k[i] = f >> 5;   // 0..15
-    b_c4[i] = f & 31;
-  }
-
-  float4 ra[2], rb[2];
+  float4 ra[kLoads], rb[kLoads];
   auto load_tile = [&](int k0) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int gr = m0 + a_row[i];
-      const int gk = k0 + a_k4[i] * 4;
+    for (int i = 0; i < kLoads; ++i) {
+      const int f = tid + THREADS * i;
+      const int gr = m0 + (f & (BM - 1));
+      const int gk = k0 + (f >> 7) * 4;
       if constexpr (!kChecked) {
         ra[i] = *reinterpret_cast<const float4*>(A + static_cast<std::uint64_t>(gr) * lda + gk);
       } else {
@@ -61,8 +56,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           v[j] = (gr < m && gk + j < k) ? A[static_cast<std::uint64_t>(gr) * lda + gk + j] : 0.f;
         ra[i] = make_float4(v[0], v[1], v[2], v[3]);
       }
-      const int bk = k0 + b_k[i];
-      const int bc = n0 + b_c4[i] * 4;
+      const int bk = k0 + (f >> 5);
+      const int bc = n0 + (f & 31) * 4;
       if constexpr (!kChecked) {
         rb[i] = *reinterpret_cast<const float4*>(B + static_cast<std::uint64_t>(bk) * ldb + bc);
       } else {
@@ -76,12 +71,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   };
   auto store_tile = [&](int buf) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      As[buf][a_k4[i] * 4 + 0][a_row[i]] = ra[i].x;
-      As[buf][a_k4[i] * 4 + 1][a_row[i]] = ra[i].y;
-      As[buf][a_k4[i] * 4 + 2][a_row[i]] = ra[i].z;
-      As[buf][a_k4[i] * 4 + 3][a_row[i]] = ra[i].w;
-      *reinterpret_cast<float4*>(&Bs[buf][b_k[i]][b_c4[i] * 4]) = rb[i];
+    for (int i = 0; i < kLoads; ++i) {
+      const int f = tid + THREADS * i;
+      const int row = f & (BM - 1), k4 = (f >> 7) * 4;
+      As[buf][k4 + 0][row] = ra[i].x;
+      As[buf][k4 + 1][row] = ra[i].y;
+      As[buf][k4 + 2][row] = ra[i].z;
+      As[buf][k4 + 3][row] = ra[i].w;
+      *reinterpret_cast<float4*>(&Bs[buf][f >> 5][(f & 31) * 4]) = rb[i];
     }
   };
 
@@ -139,6 +136,25 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+template <int BK, int MINB>
+void launch_variant(std::uint64_t m, std::uint64_t n, std::uint64_t k, const float* A,
+                    std::uint64_t lda, const float* B, std::uint64_t ldb, float* C,
+                    std::uint64_t ldc, cudaStream_t stream) {
+  const dim3 grid(static_cast<unsigned>((n + BN - 1) / BN), static_cast<unsigned>((m + BM - 1) / BM));
+  const bool aligned =
+      m % BM == 0 && n % BN == 0 && k % BK == 0 && lda % 4 == 0 && ldb % 4 == 0 &&
+      ldc % 4 == 0 &&
+      ((reinterpret_cast<std::uintptr_t>(A) | reinterpret_cast<std::uintptr_t>(B) |
+        reinterpret_cast<std::uintptr_t>(C)) & 15u) == 0;
+  if (aligned)
+    sgemm_kernel<BK, MINB, false><<<grid, THREADS, 0, stream>>>(
+        static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), A, lda, B, ldb, C, ldc);
+  else
+    sgemm_kernel<BK, MINB, true><<<grid, THREADS, 0, stream>>>(
+        static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), A, lda, B, ldb, C, ldc);
+  GPCX_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
@@ -148,25 +164,19 @@ void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
   if (m == 0 || n == 0) return;
   if (m > 0x7FFFFFFFull || n > 0x7FFFFFFFull || k > 0x7FFFFFFFull)
     fail(Errc::TooLarge, "matmul dimension exceeds 2^31");
+  if ((m + BM - 1) / BM > 65535) fail(Errc::TooLarge, "m too large for the SIMT grid");
   if (k == 0) {
     for (std::uint64_t r = 0; r < m; ++r)
       GPCX_CUDA(cudaMemsetAsync(C + r * ldc, 0, n * sizeof(float), stream));
     return;
   }
-  const dim3 grid(static_cast<unsigned>((n + BN - 1) / BN),
-                  static_cast<unsigned>((m + BM - 1) / BM));
-  const bool aligned =
-      m % BM == 0 && n % BN == 0 && k % BK == 0 && lda % 4 == 0 && ldb % 4 == 0 &&
-      ldc % 4 == 0 &&
-      ((reinterpret_cast<std::uintptr_t>(A) | reinterpret_cast<std::uintptr_t>(B) |
-        reinterpret_cast<std::uintptr_t>(C)) & 15u) == 0;
-  if (aligned)
-    sgemm_kernel<false><<<grid, THREADS, 0, stream>>>(
-        static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), A, lda, B, ldb, C, ldc);
-  else
-    sgemm_kernel<true><<<grid, THREADS, 0, stream>>>(
-        static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), A, lda, B, ldb, C, ldc);
-  GPCX_LAUNCH_CHECK();
+  const char* v = std::getenv("GPCX_SGEMM");
+  // Default BK=8 with 2 CTAs/SM: 49.6 / 50.8 TFLOP/s at 4096^3 / 8192^3 vs
+  // 47.4 / 48.5 for BK=16, 1 CTA/SM (B200, tools/mm_micro.py).
+  const std::string variant = v != nullptr ? v : "8x2";
+  if (variant == "16x1") launch_variant<16, 1>(m, n, k, A, lda, B, ldb, C, ldc, stream);
+  else if (variant == "16x2") launch_variant<16, 2>(m, n, k, A, lda, B, ldb, C, ldc, stream);
+  else launch_variant<8, 2>(m, n, k, A, lda, B, ldb, C, ldc, stream);
 }
 
 }  // namespace gpcx::gemm

@@ -36,14 +36,20 @@ def main():
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "byte": 1e-9, "Kbyte": 1e-6,
+             "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}
     kernels = []
     for r in rows[2:]:
         k = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
         for key, m in METRICS.items():
             if m in hdr:
-                v = r[hdr.index(m)]
+                i = hdr.index(m)
+                v = r[i]
                 try:
-                    k[key] = round(float(v.replace(",", "")), 4)
+                    x = float(v.replace(",", ""))
+                    if key.endswith("_ms") or key.endswith("_GB"):
+                        x *= scale.get(units[i], 1.0)
+                    k[key] = round(x, 4)
                 except ValueError:
                     k[key] = v
         kernels.append(k)
