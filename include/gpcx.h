@@ -216,6 +216,34 @@ int gpcx_synth_image_device(int kind, uint64_t seed, uint64_t rows,
 int gpcx_synth_matrix_device(int kind, uint64_t seed, uint64_t rows,
                              uint64_t cols, uint64_t row0, uint64_t nrows,
                              float* out, void* stream);
+/* BAYER_BILINEAR (gradient = 0) / BAYER_GRADIENT (gradient = 1) on a device
+ * rows x cols u16 mosaic -> out = R || G || B planes (3 * rows * cols u16);
+ * phase = 0 RGGB, 1 BGGR, 2 GRBG, 3 GBRG (gpc::img::CfaPhase order). */
+int gpcx_demosaic_device(int gradient, int phase, const uint16_t* in, uint16_t* out,
+                         uint64_t rows, uint64_t cols, void* stream);
+
+/* DEVINFO: the reference's 12-attribute record (proj/include/gpc/devinfo.hpp:23-38). */
+typedef struct gpcx_device_info {
+  char name[256];
+  char compute_capability[16];
+  int32_t warp_size;
+  uint64_t total_constant_memory;
+  uint64_t total_global_memory;
+  uint64_t shared_memory_per_block;
+  int64_t clock_rate_khz;
+  int32_t multi_processor_count;
+  int32_t registers_per_block;
+  int32_t max_threads_per_block;
+  int32_t max_grid_size[3];
+  int32_t max_threads_dim[3];
+} gpcx_device_info;
+/* Records of the bound devices (cap entries max; *count = number found). */
+int gpcx_devinfo_probe(gpcx_device_info* out, int cap, int* count);
+/* The reference's canonical XML for n records (proj/src/devinfo.cpp:94-125);
+ * *len = bytes needed (excluding the NUL); fails SIZE_MISMATCH if cap is too small. */
+int gpcx_devinfo_render(const gpcx_device_info* devs, int n, char* out, uint64_t cap,
+                        uint64_t* len);
+
 /* digest += sum_i splitmix64(((index0 + i) << 16) | v[i])  (device u64). */
 int gpcx_digest_u16_device(const uint16_t* v, uint64_t n, uint64_t index0,
                            uint64_t* digest, void* stream);

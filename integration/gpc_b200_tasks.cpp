@@ -1,8 +1,11 @@
 // gpc_b200_tasks.cpp -- see gpc_b200_tasks.hpp.
 #include "gpc_b200_tasks.hpp"
 
+#include <algorithm>
 #include <string>
+#include <vector>
 
+#include "gpc/tasks.hpp"
 #include "gpcx.h"
 
 namespace gpc::task {
@@ -50,13 +53,26 @@ TaskDescriptor b200_descriptor(const std::string& flag) {
 }  // namespace
 
 void add_b200_tasks(TaskRegistry& registry) {
-  char flags[256] = {};
+  char flags[512] = {};
   check(gpcx_flags(flags, sizeof(flags)));
+  const std::vector<std::string> have = registry.flags();
   for (std::string list = flags; !list.empty();) {
     const std::size_t comma = list.find(',');
-    registry.add(b200_descriptor(list.substr(0, comma)));
+    const std::string flag = list.substr(0, comma);
+    if (std::find(have.begin(), have.end(), flag) == have.end())
+      registry.add(b200_descriptor(flag));
     list = comma == std::string::npos ? "" : list.substr(comma + 1);
   }
+}
+
+TaskRegistry make_b200_registry(const par::ExecPlan& plan) {
+  TaskRegistry out;
+  add_b200_tasks(out);
+  const TaskRegistry cpu = make_builtin_registry(plan);
+  const std::vector<std::string> gpu = out.flags();
+  for (const std::string& flag : cpu.flags())
+    if (std::find(gpu.begin(), gpu.end(), flag) == gpu.end()) out.add(cpu.lookup(flag));
+  return out;
 }
 
 }  // namespace gpc::task

@@ -7,14 +7,23 @@
 // (proj/src/tasks.cpp:64-123).  See INTEGRATION.md.
 #pragma once
 
+#include "gpc/parexec.hpp"
 #include "gpc/registry.hpp"
 
 namespace gpc::task {
 
-// Adds the four GPU task descriptors (payload_rule -> gpcx_payload_len,
-// handler -> gpcx_output_len + gpcx_run).  Throws DuplicateFlag if a flag
-// is already registered; every gpcx failure is rethrown as the gpc::Error
-// with the same Errc, so dispatch() maps it to the same ERR:<CODE>.
+// Adds the GPU task descriptors (payload_rule -> gpcx_payload_len, handler
+// -> gpcx_output_len + gpcx_run) for every flag libgpcx serves that the
+// registry does not hold yet -- called at the end of make_builtin_registry
+// it adds LUT_GEN / LUT_APPLY / LUT_CORRECT / MATMUL and leaves the
+// built-in CPU BAYER_* / DEVINFO in place.  Every gpcx failure is rethrown
+// as the gpc::Error with the same Errc, so dispatch() maps it to the same
+// ERR:<CODE>.
 void add_b200_tasks(TaskRegistry& registry);
+
+// A registry where every flag libgpcx serves runs on the GPUs (including
+// BAYER_BILINEAR / BAYER_GRADIENT / DEVINFO) and the remaining built-ins
+// (LSQ_POLYFIT) stay on the CPU -- use it in place of make_builtin_registry.
+TaskRegistry make_b200_registry(const par::ExecPlan& plan);
 
 }  // namespace gpc::task

@@ -98,3 +98,37 @@ int refb_server_stop(void* handle) {
 }
 
 }  // extern "C"
+
+// A second reference registry built with make_b200_registry: every flag
+// libgpcx serves (BAYER_*, DEVINFO included) on the GPU, LSQ_POLYFIT on the CPU.
+namespace {
+const gpc::task::TaskRegistry& registry_gpu_first() {
+  static const gpc::task::TaskRegistry* r =
+      new gpc::task::TaskRegistry(gpc::task::make_b200_registry(gpc::par::ExecPlan{}));
+  return *r;
+}
+}  // namespace
+
+extern "C" int refb2_flags(char* out, std::size_t cap) {
+  std::string s;
+  for (const auto& f : registry_gpu_first().flags()) s += (s.empty() ? "" : ",") + f;
+  std::strncpy(out, s.c_str(), cap - 1);
+  out[cap - 1] = 0;
+  return 0;
+}
+
+extern "C" int refb2_handle_request(const std::uint8_t* req, std::size_t len, std::uint8_t* resp,
+                                    std::size_t cap, std::size_t* resp_len) {
+  try {
+    gpc::wire::MemoryStream stream(std::vector<std::uint8_t>(req, req + len));
+    gpc::srv::handle_connection(stream, registry_gpu_first());
+    const auto& w = stream.written();
+    *resp_len = w.size();
+    if (w.size() > cap) return 24;
+    std::memcpy(resp, w.data(), w.size());
+    return 0;
+  } catch (const gpc::Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  }
+}

@@ -25,6 +25,7 @@
 #include "gpc/server.hpp"
 #include "gpc/tasks.hpp"
 #include "gpc/wire.hpp"
+#include "gpcx.h"
 #include "gpcx_oracle.h"
 #include "reference.hpp"
 
@@ -337,6 +338,37 @@ int ref_submit(const char* host, int port, const char* flag, const char* params,
     *resp_len = r.payload.size();
     if (r.payload.size() > cap) fail(Errc::SizeMismatch, "response buffer too small");
     if (!r.payload.empty()) std::memcpy(resp, r.payload.data(), r.payload.size());
+  });
+}
+
+// The reference's DEVINFO XML for records given in include/gpcx.h's layout.
+int ref_devinfo_render(const gpcx_device_info* devs, int n, char* out, std::size_t cap,
+                       std::size_t* len) {
+  return guarded([&] {
+    std::vector<devinfo::DeviceInfo> list;
+    for (int i = 0; i < n; ++i) {
+      const gpcx_device_info& s = devs[i];
+      devinfo::DeviceInfo d;
+      d.name = std::string(s.name, strnlen(s.name, sizeof(s.name)));
+      d.compute_capability =
+          std::string(s.compute_capability, strnlen(s.compute_capability, sizeof(s.compute_capability)));
+      d.warp_size = s.warp_size;
+      d.total_constant_memory = s.total_constant_memory;
+      d.total_global_memory = s.total_global_memory;
+      d.shared_memory_per_block = s.shared_memory_per_block;
+      d.clock_rate_khz = s.clock_rate_khz;
+      d.multi_processor_count = s.multi_processor_count;
+      d.registers_per_block = s.registers_per_block;
+      d.max_threads_per_block = s.max_threads_per_block;
+      for (int j = 0; j < 3; ++j) {
+        d.max_grid_size[j] = s.max_grid_size[j];
+        d.max_threads_dim[j] = s.max_threads_dim[j];
+      }
+      list.push_back(d);
+    }
+    const std::string xml = devinfo::to_xml(list);
+    *len = xml.size();
+    put(xml, out, cap);
   });
 }
 

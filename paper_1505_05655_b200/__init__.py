@@ -15,10 +15,26 @@ from typing import Mapping
 import numpy as np
 
 from ._lib import (  # noqa: F401
-    EXPORTS, GpcxError, IMG_RAMP12, IMG_UNIFORM16, LIB_PATH, LUT_EQUALIZE, LUT_STRETCH,
-    LutStats, MAT_EXACT8, MAT_UNIFORM32, MODE_BY_NAME, PREC_BF16, PREC_BY_NAME, PREC_F32,
-    PREC_TF32, STATUS, check, lib,
+    EXPORTS, PHASES, DeviceInfo, GpcxError, IMG_RAMP12, IMG_UNIFORM16, LIB_PATH, LUT_EQUALIZE,
+    LUT_STRETCH, LutStats, MAT_EXACT8, MAT_UNIFORM32, MODE_BY_NAME, PREC_BF16, PREC_BY_NAME,
+    PREC_F32, PREC_TF32, STATUS, check, lib,
 )
+
+
+def devinfo_probe() -> list[DeviceInfo]:
+    arr = (DeviceInfo * 64)()
+    n = C.c_int(0)
+    check(lib.gpcx_devinfo_probe(arr, 64, C.byref(n)))
+    return list(arr[: min(n.value, 64)])
+
+
+def devinfo_render(devices: list[DeviceInfo]) -> str:
+    arr = (DeviceInfo * max(1, len(devices)))(*devices)
+    need = C.c_uint64(0)
+    lib.gpcx_devinfo_render(arr, len(devices), None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value + 1)
+    check(lib.gpcx_devinfo_render(arr, len(devices), buf, need.value + 1, C.byref(need)))
+    return buf.value.decode()
 
 __all__ = [
     "GpcxError", "init", "shutdown", "device_count", "run", "payload_len", "output_len",

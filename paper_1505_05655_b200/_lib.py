@@ -40,7 +40,19 @@ EXPORTS = [
     "gpcx_lut_apply_device", "gpcx_lut_correct_device", "gpcx_matmul_workspace_size",
     "gpcx_matmul_device", "gpcx_synth_image_device", "gpcx_synth_matrix_device",
     "gpcx_digest_u16_device", "gpcx_server_start", "gpcx_server_stop", "gpcx_handle_request",
+    "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render",
 ]
+
+PHASES = {"RGGB": 0, "BGGR": 1, "GRBG": 2, "GBRG": 3}
+
+
+class DeviceInfo(C.Structure):
+    _fields_ = [("name", C.c_char * 256), ("compute_capability", C.c_char * 16),
+                ("warp_size", C.c_int32), ("total_constant_memory", C.c_uint64),
+                ("total_global_memory", C.c_uint64), ("shared_memory_per_block", C.c_uint64),
+                ("clock_rate_khz", C.c_int64), ("multi_processor_count", C.c_int32),
+                ("registers_per_block", C.c_int32), ("max_threads_per_block", C.c_int32),
+                ("max_grid_size", C.c_int32 * 3), ("max_threads_dim", C.c_int32 * 3)]
 
 
 class LutStats(C.Structure):
@@ -97,6 +109,9 @@ def _load() -> C.CDLL:
         "gpcx_server_start": ([cp, C.c_uint16, i32, i32, C.POINTER(vp), C.POINTER(C.c_uint16)], i32),
         "gpcx_server_stop": ([vp], i32),
         "gpcx_handle_request": ([vp, u64, vp, u64, pu64], i32),
+        "gpcx_demosaic_device": ([i32, i32, vp, vp, u64, u64, vp], i32),
+        "gpcx_devinfo_probe": ([vp, i32, C.POINTER(C.c_int)], i32),
+        "gpcx_devinfo_render": ([vp, i32, cp, u64, pu64], i32),
     }
     assert set(sig) == set(EXPORTS)
     for name, (args, res) in sig.items():

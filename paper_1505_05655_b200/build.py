@@ -27,7 +27,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["lut.cu", "synth.cu", "sgemm.cu", "tc_gemm.cu"]
+CU_SOURCES = ["lut.cu", "synth.cu", "sgemm.cu", "tc_gemm.cu", "demosaic.cu"]
 CPP_SOURCES = [
     "status.cpp",
     "capi.cpp",
@@ -35,6 +35,7 @@ CPP_SOURCES = [
     "host/task_spec.cpp",
     "host/runtime.cpp",
     "host/executor.cpp",
+    "host/devinfo.cpp",
     "host/registry.cpp",
     "host/net.cpp",
     "host/server.cpp",

@@ -8,6 +8,7 @@
 
 #include "../../include/gpcx.h"
 #include "cuda_util.hpp"
+#include "host/devinfo.hpp"
 #include "host/executor.hpp"
 #include "host/registry.hpp"
 #include "host/runtime.hpp"
@@ -114,7 +115,9 @@ int gpcx_payload_len(const char* flag, const char* params, uint64_t* len) {
 int gpcx_output_len(const char* flag, const char* params, uint64_t* len) {
   return guarded([&] {
     const auto f = gpcx::task::flag_of(nz(flag));
-    *len = gpcx::task::output_len(f, gpcx::wire::ParamMap::parse(nz(params)));
+    const auto p = gpcx::wire::ParamMap::parse(nz(params));
+    *len = f == gpcx::task::Flag::DevInfo ? gpcx::exec::devinfo_xml().size()
+                                          : gpcx::task::output_len(f, p);
   });
 }
 
@@ -146,7 +149,8 @@ int gpcx_run(const char* flag, const char* params, const void* in, uint64_t in_l
   return guarded([&] {
     const auto f = gpcx::task::flag_of(nz(flag));
     const auto p = gpcx::wire::ParamMap::parse(nz(params));
-    const uint64_t want = gpcx::task::output_len(f, p);
+    const uint64_t want = f == gpcx::task::Flag::DevInfo ? gpcx::exec::devinfo_xml().size()
+                                                         : gpcx::task::output_len(f, p);
     if (out_cap < want)
       gpcx::fail(gpcx::Errc::SizeMismatch, "output buffer holds " + std::to_string(out_cap) +
                                                " bytes, need " + std::to_string(want));
@@ -321,6 +325,70 @@ int gpcx_synth_matrix_device(int kind, uint64_t seed, uint64_t rows, uint64_t co
     if (kind != GPCX_MAT_EXACT8 && kind != GPCX_MAT_UNIFORM32)
       gpcx::fail(gpcx::Errc::BadValue, "matrix kind " + std::to_string(kind));
     gpcx::synth::launch_matrix(kind, seed, rows, cols, row0, nrows, out, as_stream(stream));
+  });
+}
+
+int gpcx_demosaic_device(int gradient, int phase, const uint16_t* in, uint16_t* out,
+                         uint64_t rows, uint64_t cols, void* stream) {
+  return guarded([&] {
+    if (phase < 0 || phase > 3) gpcx::fail(gpcx::Errc::BadValue, "phase " + std::to_string(phase));
+    gpcx::demosaic::launch(gradient != 0, phase, in, out, rows, cols, as_stream(stream));
+  });
+}
+
+int gpcx_devinfo_probe(gpcx_device_info* out, int cap, int* count) {
+  return guarded([&] {
+    const auto list = gpcx::devinfo::probe_cuda(gpcx::rt::Runtime::get().devices());
+    *count = static_cast<int>(list.size());
+    for (int i = 0; i < static_cast<int>(list.size()) && i < cap; ++i) {
+      const auto& d = list[static_cast<std::size_t>(i)];
+      gpcx_device_info& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      std::strncpy(o.name, d.name.c_str(), sizeof(o.name) - 1);
+      std::strncpy(o.compute_capability, d.compute_capability.c_str(), sizeof(o.compute_capability) - 1);
+      o.warp_size = d.warp_size;
+      o.total_constant_memory = d.total_constant_memory;
+      o.total_global_memory = d.total_global_memory;
+      o.shared_memory_per_block = d.shared_memory_per_block;
+      o.clock_rate_khz = d.clock_rate_khz;
+      o.multi_processor_count = d.multi_processor_count;
+      o.registers_per_block = d.registers_per_block;
+      o.max_threads_per_block = d.max_threads_per_block;
+      for (int j = 0; j < 3; ++j) {
+        o.max_grid_size[j] = d.max_grid_size[static_cast<std::size_t>(j)];
+        o.max_threads_dim[j] = d.max_threads_dim[static_cast<std::size_t>(j)];
+      }
+    }
+  });
+}
+
+int gpcx_devinfo_render(const gpcx_device_info* devs, int n, char* out, uint64_t cap,
+                        uint64_t* len) {
+  return guarded([&] {
+    std::vector<gpcx::devinfo::DeviceInfo> list;
+    for (int i = 0; i < n; ++i) {
+      const gpcx_device_info& s = devs[i];
+      gpcx::devinfo::DeviceInfo d;
+      d.name = std::string(s.name, strnlen(s.name, sizeof(s.name)));
+      d.compute_capability =
+          std::string(s.compute_capability, strnlen(s.compute_capability, sizeof(s.compute_capability)));
+      d.warp_size = s.warp_size;
+      d.total_constant_memory = s.total_constant_memory;
+      d.total_global_memory = s.total_global_memory;
+      d.shared_memory_per_block = s.shared_memory_per_block;
+      d.clock_rate_khz = s.clock_rate_khz;
+      d.multi_processor_count = s.multi_processor_count;
+      d.registers_per_block = s.registers_per_block;
+      d.max_threads_per_block = s.max_threads_per_block;
+      for (int j = 0; j < 3; ++j) {
+        d.max_grid_size[static_cast<std::size_t>(j)] = s.max_grid_size[j];
+        d.max_threads_dim[static_cast<std::size_t>(j)] = s.max_threads_dim[j];
+      }
+      list.push_back(std::move(d));
+    }
+    const std::string xml = gpcx::devinfo::to_xml(list);
+    if (len != nullptr) *len = xml.size();
+    copy_text(xml, out, cap);
   });
 }
 

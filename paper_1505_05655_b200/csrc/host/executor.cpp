@@ -26,6 +26,7 @@
 
 #include "../cuda_util.hpp"
 #include "../kernels.hpp"
+#include "devinfo.hpp"
 #include "runtime.hpp"
 
 namespace gpcx::exec {
@@ -231,17 +232,75 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
 
 }
 
+void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
+                std::uint16_t* out) {
+  const InflightGuard inflight;
+  rt::Runtime& R = rt::Runtime::get();
+  rt::SlotLease lease = R.acquire(R.pick_device_index());
+  rt::Slot& s = *lease;
+  const std::uint64_t n = p.rows * p.cols;
+  s.a.ensure(n * 2);
+  s.c.ensure(n * 6);
+  rt::h2d(s, s.a.ptr, in, n * 2);
+  demosaic::launch(gradient, p.phase, s.a.as<std::uint16_t>(), s.c.as<std::uint16_t>(), p.rows,
+                   p.cols, s.stream);
+  rt::d2h(s, out, s.c.ptr, n * 6);
+}
+
+const std::string& devinfo_xml() {
+  // Probed once per process, like the reference's registry-time snapshot
+  // (proj/src/tasks.cpp:112-123): replays are byte-identical.
+  static const std::string* xml = [] {
+    std::vector<int> devs;
+    try {
+      devs = rt::Runtime::get().devices();
+    } catch (const Error&) {
+      devs.clear();  // no device: an empty <gpgpu_server/> inventory
+    }
+    const auto list = devinfo::probe_cuda(devs);
+    return new std::string(devinfo::to_xml(list));
+  }();
+  return *xml;
+}
+
+std::uint64_t devinfo_count() {
+  const std::string& x = devinfo_xml();
+  std::uint64_t n = 0;
+  for (std::size_t pos = x.find("<device "); pos != std::string::npos; pos = x.find("<device ", pos + 1)) ++n;
+  return n;
+}
+
 wire::ParamMap execute(Flag flag, const wire::ParamMap& params,
                        std::span<const std::uint8_t> in, std::span<std::uint8_t> out) {
   const std::uint64_t want_in = task::payload_len(flag, params);
   if (in.size() != want_in)
     fail(Errc::PayloadMismatch,
          "payload is " + std::to_string(in.size()) + " bytes, want " + std::to_string(want_in));
+  wire::ParamMap result;
+  if (flag == Flag::DevInfo) {
+    const std::string& xml = devinfo_xml();
+    if (out.size() < xml.size())
+      fail(Errc::SizeMismatch, "output buffer holds " + std::to_string(out.size()) +
+                                   " bytes, need " + std::to_string(xml.size()));
+    std::copy(xml.begin(), xml.end(), out.begin());
+    result.set("devices", devinfo_count());
+    return result;
+  }
+  if (flag == Flag::BayerBilinear || flag == Flag::BayerGradient) {
+    const task::BayerParams p = task::parse_bayer(params);
+    if (out.size() < p.rows * p.cols * 6)
+      fail(Errc::SizeMismatch, "output buffer too small for 3 planes");
+    bayer_host(flag == Flag::BayerGradient, p, reinterpret_cast<const std::uint16_t*>(in.data()),
+               reinterpret_cast<std::uint16_t*>(out.data()));
+    result.set("rows", p.rows);
+    result.set("cols", p.cols);
+    result.set("planes", std::uint64_t{3});
+    return result;
+  }
   const std::uint64_t want_out = task::output_len(flag, params);
   if (out.size() < want_out)
     fail(Errc::SizeMismatch, "output buffer holds " + std::to_string(out.size()) +
                                  " bytes, need " + std::to_string(want_out));
-  wire::ParamMap result;
   if (flag == Flag::Matmul) {
     const task::MatmulParams p = task::parse_matmul(params);
     const auto* A = reinterpret_cast<const float*>(in.data());

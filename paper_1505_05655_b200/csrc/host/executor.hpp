@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <span>
+#include <string>
 
 #include "task_spec.hpp"
 #include "wire.hpp"
@@ -25,6 +26,12 @@ gpcx_lut_stats lut_host(task::Flag flag, const task::LutParams& p, const std::ui
                         const std::uint16_t* lut_in, std::uint16_t* out,
                         std::uint16_t* lut_out);
 void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* C);
+// BAYER_BILINEAR / BAYER_GRADIENT on host buffers (out: 3 planes).
+void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
+                std::uint16_t* out);
+// DEVINFO document of the bound devices (probed once) and its device count.
+const std::string& devinfo_xml();
+std::uint64_t devinfo_count();
 
 // Work size (pixels or output rows) below which a request stays on one
 // device even when several are bound.

@@ -115,7 +115,8 @@ TaskRegistry make_b200_registry() {
     d.payload_rule = [f](const wire::ParamMap& p) { return payload_len(f, p); };
     d.handler = [f](const wire::ParamMap& p, std::span<const std::uint8_t> in) {
       TaskOutput out;
-      const std::uint64_t len = output_len(f, p);
+      const std::uint64_t len =
+          f == Flag::DevInfo ? exec::devinfo_xml().size() : output_len(f, p);
       out.pinned = rt::pinned_acquire(len);
       out.pinned_len = len;
       out.params = exec::execute(

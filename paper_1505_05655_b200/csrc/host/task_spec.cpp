@@ -8,6 +8,9 @@ Flag flag_of(std::string_view flag) {
   if (flag == "LUT_APPLY") return Flag::LutApply;
   if (flag == "LUT_CORRECT") return Flag::LutCorrect;
   if (flag == "MATMUL") return Flag::Matmul;
+  if (flag == "BAYER_BILINEAR") return Flag::BayerBilinear;
+  if (flag == "BAYER_GRADIENT") return Flag::BayerGradient;
+  if (flag == "DEVINFO") return Flag::DevInfo;
   fail(Errc::UnknownTask, std::string(flag));
 }
 
@@ -17,16 +20,22 @@ const char* flag_name(Flag f) {
     case Flag::LutApply: return "LUT_APPLY";
     case Flag::LutCorrect: return "LUT_CORRECT";
     case Flag::Matmul: return "MATMUL";
+    case Flag::BayerBilinear: return "BAYER_BILINEAR";
+    case Flag::BayerGradient: return "BAYER_GRADIENT";
+    case Flag::DevInfo: return "DEVINFO";
   }
   return "?";
 }
 
+// Sorted like the registry's std::map iteration order.
 std::vector<Flag> all_flags() {
-  return {Flag::LutApply, Flag::LutCorrect, Flag::LutGen, Flag::Matmul};
+  return {Flag::BayerBilinear, Flag::BayerGradient, Flag::DevInfo, Flag::LutApply,
+          Flag::LutCorrect,    Flag::LutGen,        Flag::Matmul};
 }
 
 std::vector<std::string> required_params(Flag f) {
   if (f == Flag::Matmul) return {"m", "k", "n"};
+  if (f == Flag::DevInfo) return {};
   return {"rows", "cols"};
 }
 
@@ -38,6 +47,11 @@ const char* prec_name(int prec) {
     case GPCX_PREC_BF16: return "bf16";
     default: return "f32";
   }
+}
+
+const char* phase_name(int phase) {
+  static const char* const kNames[4] = {"RGGB", "BGGR", "GRBG", "GBRG"};
+  return kNames[phase & 3];
 }
 
 LutParams parse_lut(Flag f, const wire::ParamMap& params) {
@@ -73,6 +87,24 @@ MatmulParams parse_matmul(const wire::ParamMap& params) {
   return p;
 }
 
+// Same order of checks as the reference handler run_demosaic
+// (proj/src/tasks.cpp:16-21): rows, cols, dtype, then phase.
+BayerParams parse_bayer(const wire::ParamMap& params) {
+  BayerParams p;
+  p.rows = params.get_uint("rows");
+  p.cols = params.get_uint("cols");
+  wire::dim_product("rows", p.rows, "cols", p.cols, 2);
+  const std::string dtype = params.get_or("dtype", "u16");
+  if (dtype != "u16") fail(Errc::BadValue, "dtype=" + dtype);
+  const std::string phase = params.get_or("phase", "RGGB");
+  if (phase == "RGGB") p.phase = 0;
+  else if (phase == "BGGR") p.phase = 1;
+  else if (phase == "GRBG") p.phase = 2;
+  else if (phase == "GBRG") p.phase = 3;
+  else fail(Errc::BadValue, "phase=" + phase);
+  return p;
+}
+
 std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
   switch (f) {
     case Flag::LutGen:
@@ -88,6 +120,16 @@ std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
       const MatmulParams p = parse_matmul(params);
       return (p.m * p.k + p.k * p.n) * 4;
     }
+    case Flag::BayerBilinear:
+    case Flag::BayerGradient: {
+      // sized like expected_payload_len's BAYER_* rule (wire.cpp:207-211):
+      // dims only; dtype / phase are the handler's to reject.
+      const std::uint64_t rows = params.get_uint("rows");
+      const std::uint64_t cols = params.get_uint("cols");
+      return wire::dim_product("rows", rows, "cols", cols, 2);
+    }
+    case Flag::DevInfo:
+      return 0;
   }
   return 0;
 }
@@ -104,6 +146,13 @@ std::uint64_t output_len(Flag f, const wire::ParamMap& params) {
       const MatmulParams p = parse_matmul(params);
       return p.m * p.n * 4;
     }
+    case Flag::BayerBilinear:
+    case Flag::BayerGradient: {
+      const BayerParams p = parse_bayer(params);
+      return p.rows * p.cols * 6;
+    }
+    case Flag::DevInfo:
+      return 0;
   }
   return 0;
 }

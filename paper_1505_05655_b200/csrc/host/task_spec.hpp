@@ -1,18 +1,22 @@
 // task_spec.hpp -- the GPU task flags: required params, payload / output
 // sizing and parameter parsing.  These are the TaskDescriptor pieces the
 // reference's built-in tasks define in proj/src/tasks.cpp:64-123 (sized_by ->
-// expected_payload_len, proj/src/wire.cpp:205-227), written for the flags of
-// SURVEY.md §8a':
+// expected_payload_len, proj/src/wire.cpp:205-227), for the flags of
+// SURVEY.md §8a' plus the §8f "next" rows:
 //
-//   flag         required       payload in                 payload out
-//   LUT_GEN      rows, cols     rows*cols u16 LE           65536 u16 LE (LUT)
-//   LUT_APPLY    rows, cols     LUT (131072 B) || image    rows*cols u16 LE
-//   LUT_CORRECT  rows, cols     rows*cols u16 LE           rows*cols u16 LE
-//   MATMUL       m, k, n        A (m*k f32) || B (k*n f32) C (m*n f32)
+//   flag            required     payload in                 payload out
+//   LUT_GEN         rows, cols   rows*cols u16 LE           65536 u16 LE (LUT)
+//   LUT_APPLY       rows, cols   LUT (131072 B) || image    rows*cols u16 LE
+//   LUT_CORRECT     rows, cols   rows*cols u16 LE           rows*cols u16 LE
+//   MATMUL          m, k, n      A (m*k f32) || B (k*n f32) C (m*n f32)
+//   BAYER_BILINEAR  rows, cols   rows*cols u16 LE mosaic    R || G || B planes
+//   BAYER_GRADIENT  rows, cols   rows*cols u16 LE mosaic    R || G || B planes
+//   DEVINFO         -            -                          XML text
 //
-// Optional: dtype=u16 and mode=equalize|stretch (LUT_GEN / LUT_CORRECT) for
-// the LUT tasks, prec=f32|tf32|bf16 for MATMUL.  Sizes follow the
-// reference's dim_product() rules and the 1 GiB kMaxPayload cap.
+// Optional: dtype=u16 and mode=equalize|stretch (LUT_GEN / LUT_CORRECT);
+// prec=f32|tf32|bf16 (MATMUL); dtype=u16, phase=RGGB|BGGR|GRBG|GBRG
+// (BAYER_*, as proj/src/tasks.cpp:13-35).  Sizes follow the reference's
+// dim_product() rules and the 1 GiB kMaxPayload cap.
 #pragma once
 
 #include <cstdint>
@@ -25,7 +29,7 @@
 
 namespace gpcx::task {
 
-enum class Flag { LutGen, LutApply, LutCorrect, Matmul };
+enum class Flag { LutGen, LutApply, LutCorrect, Matmul, BayerBilinear, BayerGradient, DevInfo };
 
 inline constexpr std::uint64_t kLutBytes = 65536 * 2;
 
@@ -43,16 +47,23 @@ struct MatmulParams {
   std::uint64_t m = 0, k = 0, n = 0;
   int prec = GPCX_PREC_F32;
 };
+struct BayerParams {
+  std::uint64_t rows = 0, cols = 0;
+  int phase = 0;  // gpc::img::CfaPhase ordinal: RGGB, BGGR, GRBG, GBRG
+};
 
-// Parse + validate (MissingParam / BadValue / Overflow).  Image byte count
-// is rows*cols*2 under the cap.
+// Parse + validate (MissingParam / BadValue / Overflow).
 LutParams parse_lut(Flag f, const wire::ParamMap& params);
 MatmulParams parse_matmul(const wire::ParamMap& params);
+BayerParams parse_bayer(const wire::ParamMap& params);
 
 std::uint64_t payload_len(Flag f, const wire::ParamMap& params);
+// DEVINFO's output length depends on the device list: callers use
+// exec::devinfo_xml() directly.
 std::uint64_t output_len(Flag f, const wire::ParamMap& params);
 
 const char* mode_name(int mode);
 const char* prec_name(int prec);
+const char* phase_name(int phase);
 
 }  // namespace gpcx::task

@@ -49,6 +49,14 @@ void launch_apply(const std::uint16_t* lut, const std::uint16_t* in,
 
 }  // namespace lut
 
+namespace demosaic {
+// BAYER_BILINEAR (gradient=false) / BAYER_GRADIENT on a rows x cols u16
+// mosaic -> 3 planes (R || G || B); phase = gpc::img::CfaPhase ordinal
+// (RGGB, BGGR, GRBG, GBRG).  BadImage below 2x2 like BayerImage::validate.
+void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
+            std::uint64_t rows, std::uint64_t cols, cudaStream_t stream);
+}  // namespace demosaic
+
 namespace synth {
 void launch_image(int kind, std::uint64_t seed, std::uint64_t rows,
                   std::uint64_t cols, std::uint64_t row0, std::uint64_t nrows,

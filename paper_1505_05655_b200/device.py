@@ -107,6 +107,14 @@ def synth_matrix(kind, seed, rows, cols, row0=0, nrows=None, out=None, stream=No
     return out
 
 
+def demosaic(gradient: bool, phase: int, mosaic, rows: int, cols: int, out=None, stream=None):
+    """3 planes (R, G, B) of rows x cols u16 (int16 tensors) from a mosaic."""
+    if out is None:
+        out = torch.empty(3 * rows * cols, dtype=torch.int16, device=mosaic.device)
+    check(lib.gpcx_demosaic_device(int(gradient), phase, _p(mosaic), _p(out), rows, cols, _s(stream)))
+    return out
+
+
 def digest_u16(v, index0=0, out=None, stream=None) -> torch.Tensor:
     if out is None:
         out = torch.zeros(1, dtype=torch.int64, device=v.device)

@@ -104,3 +104,25 @@ def test_reference_client_through_reference_server_onto_gpu(gpu, refb, refl):
         assert st == "OK"
     finally:
         refb.refb_server_stop(h)
+
+
+@pytest.mark.gpu
+def test_gpu_first_reference_registry_serves_demosaic_on_gpu(gpu, refb, refl):
+    """make_b200_registry: BAYER_* / DEVINFO on the B200 inside the reference
+    server, byte-identical to the reference's own CPU demosaic."""
+    refb.refb2_flags.argtypes = [C.c_char_p, C.c_size_t]
+    refb.refb2_handle_request.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                                          C.POINTER(C.c_size_t)]
+    buf = C.create_string_buffer(512)
+    refb.refb2_flags(buf, 512)
+    assert "LSQ_POLYFIT" in buf.value.decode() and "BAYER_GRADIENT" in buf.value.decode()
+    img = np.random.default_rng(3).integers(0, 65536, 200 * 150, dtype=np.uint32).astype(np.uint16)
+    req = W.frame("BAYER_GRADIENT", "rows=200,cols=150,phase=GRBG", img.tobytes(), "p.raw")
+    cap = 1 << 20
+    out = np.empty(cap, dtype=np.uint8)
+    n = C.c_size_t(0)
+    src = np.frombuffer(req, dtype=np.uint8)
+    assert refb.refb2_handle_request(src.ctypes.data, len(req), out.ctypes.data, cap, C.byref(n)) == 0
+    gpu_resp = out[: n.value].tobytes()
+    assert W.parse_response(gpu_resp)["status"] == "OK"
+    assert gpu_resp == refl.ref_handle_request(req)  # the reference's CPU builtin
