@@ -134,16 +134,36 @@ class Dist:
         self.n = want if self.world == 1 else self.world
         self.pg = None
 
+    # GPCX_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0 over gloo, so
+    # the N>1 code path can be exercised on a single-GPU box.
+    one_gpu = os.environ.get("GPCX_BENCH_ONE_GPU") == "1"
+
+    @property
+    def gpu(self) -> int:
+        return 0 if self.one_gpu else self.local
+
     def init(self, backend: str):
         import torch
         import torch.distributed as dist
         if self.world > 1:
-            if backend == "nccl":
+            if backend == "nccl" and not self.one_gpu:
                 torch.cuda.set_device(self.local)
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             else:
+                torch.cuda.set_device(self.gpu)
                 dist.init_process_group("gloo")
             self.pg = dist
+
+    def all_reduce_(self, t):
+        """In-place sum over ranks (NCCL on the device; via host for gloo)."""
+        if self.pg is None:
+            return
+        if self.pg.get_backend() == "nccl":
+            self.pg.all_reduce(t)
+        else:
+            h = t.cpu()
+            self.pg.all_reduce(h)
+            t.copy_(h)
 
     def barrier(self):
         if self.pg is not None:
@@ -162,6 +182,12 @@ class Dist:
             self.pg.destroy_process_group()
 
 
+def bound_devices(n: int) -> list[int]:
+    """Devices the in-process legs bind: 0..n-1 (device 0 n times in the
+    GPCX_BENCH_ONE_GPU test mode -- the planner's multi-band path)."""
+    return [0] * n if Dist.one_gpu else list(range(n))
+
+
 def band(rows: int, n: int, r: int) -> tuple[int, int]:
     per = (rows + n - 1) // n
     r0 = min(rows, r * per)
@@ -173,7 +199,7 @@ def band(rows: int, n: int, r: int) -> tuple[int, int]:
 def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     import torch
     from paper_1505_05655_b200 import device as D
-    dev = torch.device("cuda", d.local)
+    dev = torch.device("cuda", d.gpu)
     torch.cuda.set_device(dev)
     r0, nr = band(ROWS, d.n, d.rank)
     n = nr * COLS
@@ -192,7 +218,7 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
             D.lut_gen(img, mode, lut, stats, ws, stream)
         else:             # N GPUs: local histogram, NCCL all-reduce, identical LUT everywhere
             D.lut_hist(img, hist, ws, stream)
-            d.pg.all_reduce(hist)
+            d.all_reduce_(hist)
             D.lut_from_hist(hist, mode, lut, stats, ws, stream)
         if record:
             ev["h1"].append(E()); ev["h1"][-1].record(stream)
@@ -207,7 +233,7 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     d.barrier()
     torch.cuda.synchronize()
     t0, t1 = E(), E()
-    with Clocks(d.local) as clk:
+    with Clocks(d.gpu) as clk:
         t0.record(stream)
         for _ in range(steps):
             step(True)
@@ -237,7 +263,7 @@ def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int =
     import torch
     import paper_1505_05655_b200 as G
     from paper_1505_05655_b200 import device as D
-    G.init(list(range(n_gpus)))
+    G.init(bound_devices(n_gpus))
     n = ROWS * COLS
     bufs = [(G.lib.gpcx_pinned_alloc(n * 2), G.lib.gpcx_pinned_alloc(n * 2)) for _ in range(inflight)]
     try:
@@ -296,7 +322,7 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
     d.barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(d.local) as clk:
+    with Clocks(d.gpu) as clk:
         t0.record(stream)
         for _ in range(steps):
             D.matmul(prec, A, B, Cm, ws, stream)
@@ -415,7 +441,7 @@ def c5_leg(n_gpus: int) -> dict:
     server process, requests round-robined over them)."""
     import paper_1505_05655_b200 as G
     imgs, B = c5_inputs()
-    G.init(list(range(n_gpus)))
+    G.init(bound_devices(n_gpus))
     try:
         with G.Server(max_tasks=0) as srv:
             c5_run(srv.port, imgs[:8], B, "bf16")  # warm-up: slots, pinned pools

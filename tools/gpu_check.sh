@@ -1,2 +1,3 @@
-timeout 1200 python -m pytest tests/test_demosaic.py tests/test_integration.py -m gpu -q -x 2>&1 | tail -5 > gpurun_out/pytest_gpu.txt
-timeout 300 python tools/demosaic_micro.py > gpurun_out/demosaic_micro.json 2>&1
+GPCX_BENCH_ONE_GPU=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 > gpurun_out/bench_n2_onegpu.json 2> gpurun_out/bench_n2_onegpu.err
+tail -c 2000 gpurun_out/bench_n2_onegpu.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
