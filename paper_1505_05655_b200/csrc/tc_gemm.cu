@@ -361,9 +361,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // accumulator-ready commit multicasts to both CTAs' tmem_full; all 8
 // epilogue warps of the pair arrive on the leader's tmem_empty.
 
-constexpr int kStages2 = 7;
 constexpr int kStageBytes2 = 2 * 128 * 128;  // A half + B half, 16 KiB each
-constexpr int kSmemBytes2 = kStages2 * kStageBytes2 + 1024 + 256;
+template <int S>
+constexpr int smem_bytes2() {
+  return S * kStageBytes2 + 1024 + 256;
+}
 constexpr std::uint32_t kPeerMask = 0xFEFFFFFFu;  // rank bit of a shared::cluster address
 
 __device__ __forceinline__ std::uint32_t cta_rank() {
@@ -422,18 +424,19 @@ __device__ __forceinline__ void mbar_arrive_leader(std::uint64_t* bar) {
       : "memory");
 }
 
-template <bool kTf32>
+template <bool kTf32, int kStagesT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                 float* __restrict__ C, int m, int n, std::uint64_t ldc, int ktiles, int mt, int nt) {
+                 float* __restrict__ C, int m, int n, std::uint64_t ldc, int ktiles, int mt, int nt,
+                 int group_m) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~static_cast<std::uintptr_t>(1023));
   std::uint8_t* tiles = smem;
-  auto* bars = reinterpret_cast<std::uint64_t*>(smem + kStages2 * kStageBytes2);
+  auto* bars = reinterpret_cast<std::uint64_t*>(smem + kStagesT * kStageBytes2);
   std::uint64_t* full = bars;
-  std::uint64_t* empty = bars + kStages2;
-  std::uint64_t* tmem_full = bars + 2 * kStages2;
+  std::uint64_t* empty = bars + kStagesT;
+  std::uint64_t* tmem_full = bars + 2 * kStagesT;
   std::uint64_t* tmem_empty = tmem_full + 2;
   auto* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_empty + 2);
 
@@ -441,13 +444,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const std::uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const TileMap tm{mt, nt, 8};  // 256 x 256 tiles
+  const TileMap tm{mt, nt, group_m};  // 256 x 256 tiles
   const int ntiles = mt * nt;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
-    for (int s = 0; s < kStages2; ++s) {
+    for (int s = 0; s < kStagesT; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -485,7 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int kx = kb * (kTf32 ? 32 : 64);
           tma_load_2d_pair(&map_a, leader_full, sa, kx, mb * 256 + a_row0);
           tma_load_2d_pair(&map_b, leader_full, sa + 128 * 128, kx, nb * 256 + a_row0);
-          if (++stage == kStages2) {
+          if (++stage == kStagesT) {
             stage = 0;
             phase ^= 1;
           }
@@ -513,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 4; ++k)
             tc_mma_pair<kTf32>(tmem_d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           tc_commit_pair(&empty[stage]);
-          if (++stage == kStages2) {
+          if (++stage == kStagesT) {
             stage = 0;
             phase ^= 1;
           }
@@ -682,7 +685,8 @@ bool use_pair_kernel(std::uint64_t m, std::uint64_t n, std::uint64_t k, int sms)
   // panels hit L2 less (10.6 vs 4.6 GB of DRAM reads on 8192x8192x32768),
   // the extra HBM power lowers the capped clock and the 1-SM kernel wins.
   const std::uint64_t tiles2 = ((m + 255) / 256) * ((n + 255) / 256);
-  return m >= 256 && k <= 8192 && tiles2 >= static_cast<std::uint64_t>(sms / 2);
+  (void)k;
+  return m >= 256 && tiles2 >= static_cast<std::uint64_t>(sms / 2);
 }
 
 }  // namespace
@@ -730,12 +734,27 @@ void launch_tc(int prec, std::uint64_t m, std::uint64_t n, std::uint64_t k, cons
     const CUtensorMap mb = make_map(b_p, tf32, n, kp, 128);
     const int mt = static_cast<int>((m + 255) / 256), nt = static_cast<int>((n + 255) / 256);
     const int grid = 2 * std::min(mt * nt, sms / 2);
+    const char* gs = std::getenv("GPCX_TC_GROUPM");  // A/B knob (tools/, profiles/)
+    const int group_m = gs != nullptr ? std::max(1, std::atoi(gs)) : 8;
+    const char* ss = std::getenv("GPCX_TC_STAGES2");
+    // 4 stages: a deeper ring lets the CTA pairs of a wave drift apart and
+    // the shared operand panels fall out of L2 (8192x8192x32768: 4 stages
+    // 4.57 GB DRAM reads, 75.6% L2 hits; 7 stages 8.91 GB, 66.8%).
+    const int stages = ss != nullptr ? std::atoi(ss) : 4;
+    auto go = [&](auto kernel, int smem) {
+      GPCX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kernel<<<grid, kThreads, smem, stream>>>(ma, mb, C, (int)m, (int)n, ldc, ktiles, mt, nt, group_m);
+    };
     if (tf32) {
-      GPCX_CUDA(cudaFuncSetAttribute(gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2));
-      gemm2_kernel<true><<<grid, kThreads, kSmemBytes2, stream>>>(ma, mb, C, (int)m, (int)n, ldc, ktiles, mt, nt);
+      if (stages == 3) go(gemm2_kernel<true, 3>, smem_bytes2<3>());
+      else if (stages == 5) go(gemm2_kernel<true, 5>, smem_bytes2<5>());
+      else if (stages == 7) go(gemm2_kernel<true, 7>, smem_bytes2<7>());
+      else go(gemm2_kernel<true, 4>, smem_bytes2<4>());
     } else {
-      GPCX_CUDA(cudaFuncSetAttribute(gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2));
-      gemm2_kernel<false><<<grid, kThreads, kSmemBytes2, stream>>>(ma, mb, C, (int)m, (int)n, ldc, ktiles, mt, nt);
+      if (stages == 3) go(gemm2_kernel<false, 3>, smem_bytes2<3>());
+      else if (stages == 5) go(gemm2_kernel<false, 5>, smem_bytes2<5>());
+      else if (stages == 7) go(gemm2_kernel<false, 7>, smem_bytes2<7>());
+      else go(gemm2_kernel<false, 4>, smem_bytes2<4>());
     }
     GPCX_LAUNCH_CHECK();
     return;

@@ -1,3 +1,3 @@
-GPCX_BENCH_ONE_GPU=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 > gpurun_out/bench_n2_onegpu.json 2> gpurun_out/bench_n2_onegpu.err
-tail -c 2000 gpurun_out/bench_n2_onegpu.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 python -m pytest tests/test_matmul_gpu.py -q -x 2>&1 | tail -2 > gpurun_out/pytest_mm.txt
+bash tools/c4_sweep.sh > gpurun_out/c4_sweep.txt 2>&1
+GPCX_TC_KERNEL=2sm timeout 300 python tools/mm_micro.py --sizes 4096,8192,16384 --precs bf16,tf32 > gpurun_out/mm_micro_2sm.txt 2>&1

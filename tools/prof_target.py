@@ -28,6 +28,15 @@ def main():
         D.lut_correct(img, out, 0, lut, stats, ws)
         torch.cuda.synchronize()
         del img, out
+    if args.what == "longk2":  # one long-K GEMM with the caller's GPCX_TC_* environment
+        A = D.synth_matrix(1, 1, 8192, 32768)
+        B = D.synth_matrix(1, 2, 32768, 8192)
+        Cm = torch.empty(8192, 8192, device="cuda")
+        ws = D.matmul_workspace(2, 8192, 8192, 32768)
+        D.matmul(2, A, B, Cm, ws)
+        torch.cuda.synchronize()
+        print("done")
+        return
     if "longk" in args.what:  # C4-like long K, cheaper to replay than 32768^3
         import os
         m = n = 8192
