@@ -27,7 +27,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["lut.cu", "synth.cu", "sgemm.cu", "tc_gemm.cu", "demosaic.cu"]
+CU_SOURCES = ["lut.cu", "synth.cu", "sgemm.cu", "tc_gemm.cu", "demosaic.cu", "lsq.cu"]
 CPP_SOURCES = [
     "status.cpp",
     "capi.cpp",

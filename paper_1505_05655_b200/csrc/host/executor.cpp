@@ -247,6 +247,47 @@ void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* 
   rt::d2h(s, out, s.c.ptr, n * 6);
 }
 
+void lsq_host(const task::LsqParams& p, const void* y, double* out) {
+  const InflightGuard inflight;
+  if (p.pixels < 2) fail(Errc::BadValue, "pixels must be at least 2");  // ScanLineSet::validate
+  rt::Runtime& R = rt::Runtime::get();
+  rt::SlotLease lease = R.acquire(R.pick_device_index());
+  rt::Slot& s = *lease;
+  const std::uint64_t n = p.lines * p.pixels;
+  const std::uint64_t stride = lsq::kMaxOrder + 2;
+  s.a.ensure(n * (p.f32 ? 4 : 8));
+  s.b.ensure(p.lines * (stride + 4) * 8);
+  s.mm_ws.ensure(lsq::workspace_bytes(p.lines, p.pixels));
+  rt::h2d(s, s.a.ptr, y, n * (p.f32 ? 4 : 8));
+  auto* coeffs = s.b.as<double>();
+  double* status = coeffs + p.lines * stride;
+  lsq::launch(s.a.ptr, p.f32, p.lines, p.pixels, p.order, coeffs, status, s.mm_ws.ptr, s.stream);
+  std::vector<double> host(p.lines * (stride + 4));
+  rt::d2h(s, host.data(), coeffs, host.size() * 8);
+  const double* hst = host.data() + p.lines * stride;
+  // First failing line, worded like the reference's batch_fit +
+  // fits_to_le_bytes (proj/src/lsq.cpp:198-273).
+  for (std::uint64_t line = 0; line < p.lines; ++line) {
+    const double* st = hst + line * 4;
+    const std::string where = "line " + std::to_string(line) + ": ";
+    if (st[0] == 1.0)
+      fail(Errc::TaskFailed, where + where + "non-finite sample at " +
+                                 std::to_string(static_cast<std::uint64_t>(st[1])));
+    if (st[0] == 2.0)
+      fail(Errc::TaskFailed, where + std::to_string(p.pixels) + " points for order " +
+                                 std::to_string(p.order));
+    if (st[0] == 3.0)
+      fail(Errc::TaskFailed, where + "pivot " + std::to_string(static_cast<int>(st[1])) + " is " +
+                                 std::to_string(st[2]) + ", floor " + std::to_string(st[3]));
+  }
+  const std::uint64_t m2 = static_cast<std::uint64_t>(p.order) + 2;
+  for (std::uint64_t line = 0; line < p.lines; ++line) {
+    const double* src = host.data() + line * stride;
+    for (std::uint64_t k = 0; k + 1 < m2; ++k) out[line * m2 + k] = src[k];
+    out[line * m2 + m2 - 1] = src[p.order + 1];
+  }
+}
+
 const std::string& devinfo_xml() {
   // Probed once per process, like the reference's registry-time snapshot
   // (proj/src/tasks.cpp:112-123): replays are byte-identical.
@@ -284,6 +325,15 @@ wire::ParamMap execute(Flag flag, const wire::ParamMap& params,
                                    " bytes, need " + std::to_string(xml.size()));
     std::copy(xml.begin(), xml.end(), out.begin());
     result.set("devices", devinfo_count());
+    return result;
+  }
+  if (flag == Flag::LsqPolyfit) {
+    const task::LsqParams p = task::parse_lsq(params);
+    const std::uint64_t want = p.lines * (static_cast<std::uint64_t>(p.order) + 2) * 8;
+    if (out.size() < want) fail(Errc::SizeMismatch, "output buffer too small for the fits");
+    lsq_host(p, in.data(), reinterpret_cast<double*>(out.data()));
+    result.set("lines", p.lines);
+    result.set("order", static_cast<std::uint64_t>(p.order));
     return result;
   }
   if (flag == Flag::BayerBilinear || flag == Flag::BayerGradient) {

@@ -29,6 +29,8 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
 // BAYER_BILINEAR / BAYER_GRADIENT on host buffers (out: 3 planes).
 void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
                 std::uint16_t* out);
+// LSQ_POLYFIT on host buffers: out = lines x (order + 2) doubles.
+void lsq_host(const task::LsqParams& p, const void* y, double* out);
 // DEVINFO document of the bound devices (probed once) and its device count.
 const std::string& devinfo_xml();
 std::uint64_t devinfo_count();

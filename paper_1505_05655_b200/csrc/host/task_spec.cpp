@@ -11,6 +11,7 @@ Flag flag_of(std::string_view flag) {
   if (flag == "BAYER_BILINEAR") return Flag::BayerBilinear;
   if (flag == "BAYER_GRADIENT") return Flag::BayerGradient;
   if (flag == "DEVINFO") return Flag::DevInfo;
+  if (flag == "LSQ_POLYFIT") return Flag::LsqPolyfit;
   fail(Errc::UnknownTask, std::string(flag));
 }
 
@@ -23,20 +24,36 @@ const char* flag_name(Flag f) {
     case Flag::BayerBilinear: return "BAYER_BILINEAR";
     case Flag::BayerGradient: return "BAYER_GRADIENT";
     case Flag::DevInfo: return "DEVINFO";
+    case Flag::LsqPolyfit: return "LSQ_POLYFIT";
   }
   return "?";
 }
 
 // Sorted like the registry's std::map iteration order.
 std::vector<Flag> all_flags() {
-  return {Flag::BayerBilinear, Flag::BayerGradient, Flag::DevInfo, Flag::LutApply,
-          Flag::LutCorrect,    Flag::LutGen,        Flag::Matmul};
+  return {Flag::BayerBilinear, Flag::BayerGradient, Flag::DevInfo,    Flag::LsqPolyfit,
+          Flag::LutApply,      Flag::LutCorrect,    Flag::LutGen,     Flag::Matmul};
 }
 
 std::vector<std::string> required_params(Flag f) {
   if (f == Flag::Matmul) return {"m", "k", "n"};
   if (f == Flag::DevInfo) return {};
+  if (f == Flag::LsqPolyfit) return {"lines", "pixels", "order"};
   return {"rows", "cols"};
+}
+
+LsqParams parse_lsq(const wire::ParamMap& params) {
+  LsqParams p;
+  p.lines = params.get_uint("lines");
+  p.pixels = params.get_uint("pixels");
+  const std::uint64_t order = params.get_uint("order");
+  if (order > 8)
+    fail(Errc::OrderTooHigh, "order " + std::to_string(order) + " exceeds 8");
+  p.order = static_cast<int>(order);
+  const std::string dtype = params.get_or("dtype", "f64");
+  if (dtype == "f32") p.f32 = true;
+  else if (dtype != "f64") fail(Errc::BadValue, "dtype=" + dtype);
+  return p;
 }
 
 const char* mode_name(int mode) { return mode == GPCX_LUT_STRETCH ? "stretch" : "equalize"; }
@@ -130,6 +147,18 @@ std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
     }
     case Flag::DevInfo:
       return 0;
+    case Flag::LsqPolyfit: {
+      // expected_payload_len's LSQ_POLYFIT rule (wire.cpp:212-224): dtype is
+      // checked here, before the payload, order only by the handler.
+      const std::uint64_t lines = params.get_uint("lines");
+      const std::uint64_t pixels = params.get_uint("pixels");
+      const std::string dtype = params.get_or("dtype", "f64");
+      std::uint64_t scale = 0;
+      if (dtype == "f32") scale = 4;
+      else if (dtype == "f64") scale = 8;
+      else fail(Errc::BadValue, "dtype=" + dtype);
+      return wire::dim_product("lines", lines, "pixels", pixels, scale);
+    }
   }
   return 0;
 }
@@ -153,6 +182,10 @@ std::uint64_t output_len(Flag f, const wire::ParamMap& params) {
     }
     case Flag::DevInfo:
       return 0;
+    case Flag::LsqPolyfit: {
+      const LsqParams p = parse_lsq(params);
+      return p.lines * (static_cast<std::uint64_t>(p.order) + 2) * 8;
+    }
   }
   return 0;
 }

@@ -29,7 +29,11 @@
 
 namespace gpcx::task {
 
-enum class Flag { LutGen, LutApply, LutCorrect, Matmul, BayerBilinear, BayerGradient, DevInfo };
+//   LSQ_POLYFIT     lines, pixels, lines*pixels f32/f64 LE  per line a_0..a_m, SSE (f64)
+//                   order
+enum class Flag {
+  LutGen, LutApply, LutCorrect, Matmul, BayerBilinear, BayerGradient, DevInfo, LsqPolyfit
+};
 
 inline constexpr std::uint64_t kLutBytes = 65536 * 2;
 
@@ -52,8 +56,17 @@ struct BayerParams {
   int phase = 0;  // gpc::img::CfaPhase ordinal: RGGB, BGGR, GRBG, GBRG
 };
 
+struct LsqParams {
+  std::uint64_t lines = 0, pixels = 0;
+  int order = 0;
+  bool f32 = false;
+};
+
 // Parse + validate (MissingParam / BadValue / Overflow).
 LutParams parse_lut(Flag f, const wire::ParamMap& params);
+// The reference handler's order (proj/src/tasks.cpp:37-60): lines, pixels,
+// order (OrderTooHigh above 8), dtype.
+LsqParams parse_lsq(const wire::ParamMap& params);
 MatmulParams parse_matmul(const wire::ParamMap& params);
 BayerParams parse_bayer(const wire::ParamMap& params);
 

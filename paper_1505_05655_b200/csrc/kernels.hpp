@@ -57,6 +57,18 @@ void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* ou
             std::uint64_t rows, std::uint64_t cols, cudaStream_t stream);
 }  // namespace demosaic
 
+namespace lsq {
+inline constexpr int kMaxOrder = 8;  // gpc::lsq::kMaxOrder
+// Per-line polynomial fits of `lines` x `pixels` samples (f32 or f64,
+// device memory).  out_coeffs: lines x (kMaxOrder + 2) doubles, the first
+// order+1 the coefficients (constant first) then the SSE; out_status:
+// lines x 4 doubles {code (0 ok, 1 non-finite, 2 insufficient points,
+// 3 singular), col / index, best pivot, pivot floor}.
+std::uint64_t workspace_bytes(std::uint64_t lines, std::uint64_t pixels);
+void launch(const void* y, bool dtype_f32, std::uint64_t lines, std::uint64_t pixels, int order,
+            double* out_coeffs, double* out_status, void* ws, cudaStream_t stream);
+}  // namespace lsq
+
 namespace synth {
 void launch_image(int kind, std::uint64_t seed, std::uint64_t rows,
                   std::uint64_t cols, std::uint64_t row0, std::uint64_t nrows,

@@ -30,8 +30,9 @@ def test_every_declared_symbol_is_exported():
 
 def test_abi_version_and_flags():
     assert G.lib.gpcx_abi_version() == 1
-    assert G.flags() == ["BAYER_BILINEAR", "BAYER_GRADIENT", "DEVINFO", "LUT_APPLY", "LUT_CORRECT",
-                         "LUT_GEN", "MATMUL"]
+    assert G.flags() == ["BAYER_BILINEAR", "BAYER_GRADIENT", "DEVINFO", "LSQ_POLYFIT", "LUT_APPLY",
+                         "LUT_CORRECT", "LUT_GEN", "MATMUL"]
+    assert G.required_params("LSQ_POLYFIT") == ["lines", "pixels", "order"]
     assert G.required_params("DEVINFO") == []
     assert G.required_params("BAYER_GRADIENT") == ["rows", "cols"]
     assert G.required_params("LUT_CORRECT") == ["rows", "cols"]
