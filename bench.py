@@ -407,17 +407,23 @@ def c5_inputs() -> tuple[list[bytes], bytes]:
 
 def c5_chain(port: int, img: bytes, B: bytes, prec: str) -> int:
     """LUT_GEN -> LUT_APPLY (image correction) -> MATMUL on the corrected
-    image's top-left 1024^2 block; returns the bytes moved over TCP."""
-    from paper_1505_05655_b200.client import submit
+    image's top-left block; returns the bytes moved over TCP.  The client is
+    libgpcx's native one (gpcx_client_submit, the reference client's
+    protocol) so the load generator's socket I/O runs off the GIL."""
+    from paper_1505_05655_b200.client import submit_native as submit
     dims = f"rows={C5_IMG},cols={C5_IMG}"
-    r1 = submit("127.0.0.1", port, "LUT_GEN", dims, img, "lut.bin")
+    lut = np.empty(131072, dtype=np.uint8)
+    r1 = submit("127.0.0.1", port, "LUT_GEN", dims, [img], output_name="lut.bin", out=lut)
     assert r1.ok, r1.status
-    r2 = submit("127.0.0.1", port, "LUT_APPLY", dims, [r1.payload, img], "img.raw")
+    corr = np.empty(C5_IMG * C5_IMG, dtype=np.uint16)
+    r2 = submit("127.0.0.1", port, "LUT_APPLY", dims, [lut, img], output_name="img.raw",
+                out=corr.view(np.uint8))
     assert r2.ok, r2.status
-    corr = np.frombuffer(r2.payload, dtype=np.uint16).reshape(C5_IMG, C5_IMG)
-    A = corr[:C5_MM, :C5_MM].astype(np.float32)
+    A = corr.reshape(C5_IMG, C5_IMG)[:C5_MM, :C5_MM].astype(np.float32)
     A *= np.float32(1.0 / 65535.0)
-    r3 = submit("127.0.0.1", port, "MATMUL", f"m={C5_MM},k={C5_MM},n={C5_MM},prec={prec}", [A, B], "c.f32")
+    cm = np.empty(C5_MM * C5_MM, dtype=np.float32)
+    r3 = submit("127.0.0.1", port, "MATMUL", f"m={C5_MM},k={C5_MM},n={C5_MM},prec={prec}", [A, B],
+                output_name="c.f32", out=cm.view(np.uint8))
     assert r3.ok, r3.status
     return (len(img) * 2 + len(r1.payload) + A.nbytes + len(B) + len(r1.payload) + len(r2.payload)
             + len(r3.payload) + 6 * 260)
@@ -451,7 +457,7 @@ def c5_leg(n_gpus: int) -> dict:
     res.update({"workload": f"C5: {C5_REQUESTS} concurrent clients x (LUT_GEN -> LUT_APPLY -> "
                             f"MATMUL prec=bf16), {C5_IMG}^2 u16 images, {C5_MM}^3 matmul",
                 "server": "gpcx B200 server (max_tasks = 2 x hw threads), loopback TCP, "
-                          "Python wire client"})
+                          "native client (gpcx_client_submit) driven from 64 threads"})
     return res
 
 

@@ -267,6 +267,20 @@ int gpcx_server_stop(void* handle);
 int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp,
                         uint64_t resp_cap, uint64_t* resp_len);
 
+/* Client side (the reference's client::submit, proj/src/client.cpp:97-129):
+ * one request over one TCP connection.  The payload is the concatenation of
+ * nparts buffers (parts[i], part_len[i]) -- e.g. LUT || image without a
+ * copy.  The response payload lands in resp (resp_cap bytes; *resp_len =
+ * its size, SIZE_MISMATCH if it does not fit); status and params are
+ * written NUL-terminated into the given buffers (64 and 256 bytes
+ * suffice).  An ERR:<CODE> response is data (returns OK);
+ * transport failures return CONNECT_FAILED / TRUNCATED / IO_ERROR. */
+int gpcx_client_submit(const char* host, uint16_t port, const char* flag, const char* params,
+                       const void* const* parts, const uint64_t* part_len, int nparts,
+                       const char* output_name, void* resp, uint64_t resp_cap,
+                       uint64_t* resp_len, char* status, uint64_t status_cap,
+                       char* resp_params, uint64_t resp_params_cap);
+
 #ifdef __cplusplus
 }
 #endif

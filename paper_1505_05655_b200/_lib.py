@@ -40,7 +40,7 @@ EXPORTS = [
     "gpcx_lut_apply_device", "gpcx_lut_correct_device", "gpcx_matmul_workspace_size",
     "gpcx_matmul_device", "gpcx_synth_image_device", "gpcx_synth_matrix_device",
     "gpcx_digest_u16_device", "gpcx_server_start", "gpcx_server_stop", "gpcx_handle_request",
-    "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render",
+    "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render", "gpcx_client_submit",
 ]
 
 PHASES = {"RGGB": 0, "BGGR": 1, "GRBG": 2, "GBRG": 3}
@@ -112,6 +112,8 @@ def _load() -> C.CDLL:
         "gpcx_demosaic_device": ([i32, i32, vp, vp, u64, u64, vp], i32),
         "gpcx_devinfo_probe": ([vp, i32, C.POINTER(C.c_int)], i32),
         "gpcx_devinfo_render": ([vp, i32, cp, u64, pu64], i32),
+        "gpcx_client_submit": ([cp, C.c_uint16, cp, cp, C.POINTER(vp), pu64, i32, cp, vp, u64, pu64,
+                                cp, u64, cp, u64], i32),
     }
     assert set(sig) == set(EXPORTS)
     for name, (args, res) in sig.items():

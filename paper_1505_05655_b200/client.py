@@ -53,6 +53,37 @@ def _recv_exact(s: socket.socket, n: int) -> bytearray:
     return buf
 
 
+def submit_native(host: str, port: int, flag: str, params, parts=(), resp_cap: int = 0,
+                  output_name: str = "", out=None) -> TaskResult:
+    """The same request through libgpcx's C++ client (gpcx_client_submit):
+    socket I/O off the GIL, payload parts sent without concatenation, the
+    response written into `out` (a writable buffer of >= resp_cap bytes) or
+    a new bytearray."""
+    import ctypes as C
+
+    import numpy as np
+
+    from ._lib import check, lib
+    text = _params_text(params)
+    arrays = [np.frombuffer(memoryview(p).cast("B"), dtype=np.uint8) for p in parts]
+    ptrs = (C.c_void_p * max(1, len(arrays)))(*[a.ctypes.data for a in arrays])
+    lens = (C.c_uint64 * max(1, len(arrays)))(*[a.nbytes for a in arrays])
+    if out is None:
+        out = bytearray(resp_cap)
+    ob = (C.c_char * len(out)).from_buffer(out) if len(out) else None
+    got = C.c_uint64(0)
+    status = C.create_string_buffer(64)
+    rparams = C.create_string_buffer(256)
+    check(lib.gpcx_client_submit(host.encode(), port, flag.encode(), text.encode(), ptrs, lens,
+                                 len(arrays), output_name.encode(), ob, len(out), C.byref(got),
+                                 status, 64, rparams, 256))
+    params_out = {}
+    for tok in filter(None, rparams.value.decode().split(",")):
+        k, _, v = tok.partition("=")
+        params_out[k] = v.replace(";", ",")
+    return TaskResult(status.value.decode(), params_out, memoryview(out)[: got.value], output_name)
+
+
 def submit(host: str, port: int, flag: str, params, payload=b"",
            output_name: str = "", timeout: float = 300.0) -> TaskResult:
     """`payload` is bytes-like or a list of bytes-like parts sent back to

@@ -10,6 +10,7 @@
 #include "cuda_util.hpp"
 #include "host/devinfo.hpp"
 #include "host/executor.hpp"
+#include "host/net.hpp"
 #include "host/registry.hpp"
 #include "host/runtime.hpp"
 #include "host/server.hpp"
@@ -443,6 +444,40 @@ int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp, uin
       gpcx::fail(gpcx::Errc::SizeMismatch, "response buffer holds " + std::to_string(resp_cap) +
                                                " bytes, need " + std::to_string(bytes.size()));
     if (!bytes.empty()) std::memcpy(resp, bytes.data(), bytes.size());
+  });
+}
+
+int gpcx_client_submit(const char* host, uint16_t port, const char* flag, const char* params,
+                       const void* const* parts, const uint64_t* part_len, int nparts,
+                       const char* output_name, void* resp, uint64_t resp_cap,
+                       uint64_t* resp_len, char* status, uint64_t status_cap,
+                       char* resp_params, uint64_t resp_params_cap) {
+  return guarded([&] {
+    std::uint64_t total = 0;
+    for (int i = 0; i < nparts; ++i) total += part_len[i];
+    gpcx::wire::TaskHeader h;
+    h.task_flag = nz(flag);
+    h.params = gpcx::wire::ParamMap::parse(nz(params)).serialize();
+    h.output_name = nz(output_name);
+    h.data_marker = total > 0 ? gpcx::wire::kMarkerData : gpcx::wire::kMarkerNone;
+    if (total > gpcx::wire::kMaxPayload) gpcx::fail(gpcx::Errc::TooLarge, "payload over the cap");
+    const gpcx::wire::HeaderBytes raw = gpcx::wire::encode_header(h);
+    gpcx::net::Socket s = gpcx::net::Socket::connect_to(nz(host), port);
+    s.write_all(raw);
+    for (int i = 0; i < nparts; ++i)
+      if (part_len[i] > 0)
+        s.write_all(std::span<const std::uint8_t>(static_cast<const std::uint8_t*>(parts[i]), part_len[i]));
+    gpcx::wire::HeaderBytes rh;
+    gpcx::wire::read_exact(s, rh);
+    const gpcx::wire::TaskHeader r = gpcx::wire::decode_header(rh);
+    const std::uint64_t n = gpcx::wire::response_payload_len(r);
+    if (resp_len != nullptr) *resp_len = n;
+    if (n > resp_cap)
+      gpcx::fail(gpcx::Errc::SizeMismatch, "response payload is " + std::to_string(n) +
+                                               " bytes, buffer holds " + std::to_string(resp_cap));
+    if (n > 0) gpcx::wire::read_exact(s, std::span<std::uint8_t>(static_cast<std::uint8_t*>(resp), n));
+    copy_text(r.task_flag, status, status_cap);
+    copy_text(r.params, resp_params, resp_params_cap);
   });
 }
 

@@ -148,3 +148,14 @@ def test_many_concurrent_gpu_requests(gpu, server, refl):
     [t.start() for t in ts]
     [t.join() for t in ts]
     assert not errors, errors
+
+
+def test_native_client_round_trips_errors_like_reference_client(server, refl):
+    from paper_1505_05655_b200.client import submit_native
+    for flag, params in [("NOPE", "a=1"), ("LUT_CORRECT", "rows=4"), ("MATMUL", "m=1,k=1,n=1,prec=q")]:
+        ours = submit_native("127.0.0.1", server.port, flag, params, [b"\x01\x02"], 0, "n.bin")
+        st, p, _, _ = refl.ref_submit(server.port, flag, params, b"\x01\x02", "n.bin")
+        assert ours.status == st and ours.params == G.parse_params(p)
+    with pytest.raises(G.GpcxError) as e:
+        submit_native("127.0.0.1", 1, "NOPE", "", [], 0)
+    assert e.value.code == "ConnectFailed"

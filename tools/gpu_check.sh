@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_lsq.py tests/test_integration.py -m gpu -q -x 2>&1 | tail -25 > gpurun_out/pytest_gpu.txt
+timeout 1200 python bench.py --steps 10 --warmup 3 --workload c5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+tail -c 600 gpurun_out/bench_c5.err
