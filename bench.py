@@ -562,7 +562,10 @@ def run_b200(args) -> None:
                        "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
                        "parallelism": f"row-band x{d.n}, NCCL all-reduce of the 65536-bin histogram",
                        "l2": "inputs larger than L2 (2 GiB scene)"},
-            "roofline": roof, "gpu_launches": 4 * args.steps, "clocks": lut["clocks"]}
+            # per step: hist_kernel + build_kernel + apply_kernel at N=1;
+            # N>1 adds merge_kernel (the local histogram leaves the device for NCCL)
+            "roofline": roof, "gpu_launches": (3 if d.n == 1 else 4) * args.steps,
+            "clocks": lut["clocks"]}
     e2e_steps = max(4, min(args.steps, 8))
     e2e1 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=1)
     e2e2 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=2)

@@ -71,7 +71,7 @@ class GpcxError(RuntimeError):
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1505_05655_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1505_05655_b200/build.py` "
             "(there is no CPU fallback)")
     lib = C.CDLL(str(LIB_PATH))
     u64, u32, vp, cp, i32 = C.c_uint64, C.c_uint32, C.c_void_p, C.c_char_p, C.c_int

@@ -9,7 +9,8 @@
 //             device builds the identical LUT and applies it to its band,
 //             and each band is DMA'd straight into its disjoint slice of the
 //             host response buffer -- that D2H is the gather.
-//   MATMUL  : block rows of A and C, B replicated; tile / K order do not
+//   MATMUL  : block rows of A and C, B replicated (each device stages 1/G of
+//             B from the host and copies the rest from its peers); tile / K order do not
 //             depend on G, so C is bitwise identical for any device count
 //             (the analogue of acceptance.cpp:278-315's worker invariance).
 #include "executor.hpp"
@@ -209,16 +210,40 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
   std::vector<rt::SlotLease> leases;
   leases.reserve(G);
   for (const Band& b : bands) leases.push_back(R.acquire(b.dev_index));
+  // B is replicated by slices: device i stages only rows
+  // [ks[i], ks[i+1]) of B over its own PCIe link, then pulls the other
+  // slices from its peers over NVLink -- G-fold less host->device traffic
+  // for B than every device copying all of it.
+  std::vector<std::uint64_t> ks(G + 1, 0);
+  for (std::size_t i = 0; i <= G; ++i) ks[i] = std::min<std::uint64_t>(p.k, (p.k + G - 1) / G * i);
+  const std::uint64_t row_bytes = p.n * 4;
 
   for_each_band(G, [&](std::size_t i) {
     rt::Slot& s = *leases[i];
     rt::use_device(s.device);
     const Band& b = bands[i];
     s.a.ensure(std::max<std::uint64_t>(b.nrows * p.k * 4, 4));
-    s.b.ensure(std::max<std::uint64_t>(p.k * p.n * 4, 4));
+    s.b.ensure(std::max<std::uint64_t>(p.k * row_bytes, 4));
     s.c.ensure(std::max<std::uint64_t>(b.nrows * p.n * 4, 4));
+    rt::h2d(s, s.b.as<std::uint8_t>() + ks[i] * row_bytes,
+            reinterpret_cast<const std::uint8_t*>(B) + ks[i] * row_bytes,
+            (ks[i + 1] - ks[i]) * row_bytes);
+    GPCX_CUDA(cudaEventRecord(s.ready, s.stream));
     rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
-    rt::h2d(s, s.b.ptr, B, p.k * p.n * 4);
+  });
+
+  for_each_band(G, [&](std::size_t i) {
+    rt::Slot& s = *leases[i];
+    rt::use_device(s.device);
+    const Band& b = bands[i];
+    for (std::size_t j = 0; j < G; ++j) {
+      if (j == i || ks[j + 1] == ks[j]) continue;
+      const rt::Slot& peer = *leases[j];
+      GPCX_CUDA(cudaStreamWaitEvent(s.stream, peer.ready, 0));
+      GPCX_CUDA(cudaMemcpyPeerAsync(s.b.as<std::uint8_t>() + ks[j] * row_bytes, s.device,
+                                    peer.b.as<std::uint8_t>() + ks[j] * row_bytes, peer.device,
+                                    (ks[j + 1] - ks[j]) * row_bytes, s.stream));
+    }
     if (p.prec == GPCX_PREC_F32) {
       gemm::launch_sgemm(b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,
                          s.c.as<float>(), p.n, s.stream);
@@ -227,9 +252,11 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
       gemm::launch_tc(p.prec, b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,
                       s.c.as<float>(), p.n, s.mm_ws.ptr, s.stream);
     }
+    // A peer may still be reading this device's B slice; every band's d2h
+    // synchronises its own stream, and for_each_band joins them all before
+    // any slot (and its B) returns to the pool.
     rt::d2h(s, outb + b.row0 * p.n * 4, s.c.ptr, b.nrows * p.n * 4);
   });
-
 }
 
 void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,

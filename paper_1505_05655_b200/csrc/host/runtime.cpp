@@ -54,6 +54,7 @@ Slot::~Slot() {
   h_small.release();
   for (cudaEvent_t& e : chunk_done)
     if (e != nullptr) cudaEventDestroy(e);
+  if (ready != nullptr) cudaEventDestroy(ready);
   if (stream != nullptr) cudaStreamDestroy(stream);
 }
 
@@ -65,6 +66,26 @@ Runtime& Runtime::get() {
   static Runtime* rt = new Runtime();  // never destroyed: outlives static teardown
   return *rt;
 }
+
+namespace {
+// Direct NVLink access between every pair of bound devices, so a peer copy
+// (cudaMemcpyPeerAsync) is one DMA over NVSwitch instead of a host bounce.
+// Best effort: without it the copies still work, just staged.
+void enable_peer_access(const std::vector<int>& devs) {
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  for (int d : devs) {
+    for (int p : devs) {
+      if (p == d) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, d, p) != cudaSuccess || !can) continue;
+      cudaSetDevice(d);
+      if (cudaDeviceEnablePeerAccess(p, 0) != cudaSuccess) cudaGetLastError();
+    }
+  }
+  cudaSetDevice(cur);
+}
+}  // namespace
 
 void Runtime::init(const std::vector<int>& devices) {
   std::lock_guard<std::mutex> lock(mu_);
@@ -85,6 +106,7 @@ void Runtime::init(const std::vector<int>& devices) {
     if (d < 0 || d >= count) fail(Errc::BadValue, "device " + std::to_string(d) + " not present");
     pools_.push_back(Pool{d, {}, {}});
   }
+  enable_peer_access(want);
   inited_ = true;
 }
 
@@ -99,7 +121,12 @@ void Runtime::ensure_init_locked() {
   int count = 0;
   GPCX_CUDA(cudaGetDeviceCount(&count));
   if (count <= 0) fail(Errc::TaskFailed, "no CUDA device available");
-  for (int i = 0; i < count; ++i) pools_.push_back(Pool{i, {}, {}});
+  std::vector<int> all;
+  for (int i = 0; i < count; ++i) {
+    pools_.push_back(Pool{i, {}, {}});
+    all.push_back(i);
+  }
+  enable_peer_access(all);
   inited_ = true;
 }
 
@@ -110,6 +137,8 @@ std::vector<int> Runtime::devices() {
   for (const Pool& p : pools_) out.push_back(p.device);
   return out;
 }
+
+int Runtime::device_at(int index) { return devices().at(static_cast<std::size_t>(index)); }
 
 int Runtime::ndev() { return static_cast<int>(devices().size()); }
 
@@ -137,6 +166,7 @@ SlotLease Runtime::acquire(int device_index) {
   GPCX_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
   for (cudaEvent_t& e : slot->chunk_done)
     GPCX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  GPCX_CUDA(cudaEventCreateWithFlags(&slot->ready, cudaEventDisableTiming));
   slot->small.ensure(131072 + 256 + 65536 * 4);
   slot->h_small.ensure(256);
   slot->lut_ws.ensure(lut::workspace_bytes(), /*zero=*/true);

@@ -47,6 +47,7 @@ struct Slot {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t chunk_done[2] = {nullptr, nullptr};
+  cudaEvent_t ready = nullptr;  // cross-device handoff (e.g. a staged B slice)
   DeviceBuf a, b, c;     // operands / result
   DeviceBuf lut_ws;      // LUT workspace (zeroed once, self-cleaning)
   DeviceBuf mm_ws;       // tensor-core matmul workspace
@@ -91,6 +92,8 @@ class Runtime {
   std::vector<int> devices();
   int ndev();
   int pick_device_index();  // round robin over bound devices (C5 replicas)
+  // Device ordinal of bound index i.
+  int device_at(int index);
   SlotLease acquire(int device_index);
   void release(Slot* slot);
 

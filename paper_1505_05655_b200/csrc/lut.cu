@@ -240,93 +240,6 @@ __device__ __forceinline__ uint32_t stretch_entry(std::uint64_t v,
       udiv_exact((v - lo) * 65535u + span / 2, span, 1.0 / static_cast<double>(span)));
 }
 
-// Equalize (or stretch, from the histogram's extremes) LUT.  One CTA of 32
-// warps; warp w owns bins [2048w, 2048w + 2048) and walks them 32 at a time
-// with coalesced 128-byte loads.  Pass 1: per-warp totals and first / last
-// non-empty bin; a 32-entry scan gives every warp its cdf offset.  Pass 2:
-// warp-shuffle inclusive scan of each 32-bin row -> cdf -> LUT entries,
-// written as coalesced 64-byte rows.
-__global__ void __launch_bounds__(1024, 1)
-    from_hist_kernel(const uint32_t* __restrict__ hist, int mode,
-                     std::uint16_t* __restrict__ lut,
-                     gpcx_lut_stats* __restrict__ stats) {
-  constexpr int kRows = kBins / 1024;  // 64 rows of 32 bins per warp
-  __shared__ uint32_t s_tot[32], s_lo[32], s_hi[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t base = static_cast<uint32_t>(warp) * (kRows * 32);
-  const uint32_t* hw = hist + base + lane;
-
-  uint32_t acc = 0, first = 0xFFFFFFFFu, last = 0;
-#pragma unroll 8
-  for (int r = 0; r < kRows; ++r) {
-    const uint32_t x = __ldg(hw + r * 32);
-    acc += x;
-    if (x != 0) {
-      first = min(first, base + r * 32 + lane);
-      last = base + r * 32 + lane;
-    }
-  }
-  const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, acc);
-  const uint32_t wlo = __reduce_min_sync(0xFFFFFFFFu, first);
-  const uint32_t whi = __reduce_max_sync(0xFFFFFFFFu, last);
-  if (lane == 0) {
-    s_tot[warp] = wtot;
-    s_lo[warp] = wlo;
-    s_hi[warp] = wtot != 0 ? whi : 0;
-  }
-  __syncthreads();
-  // every warp redoes the 32-entry reductions (cheaper than another barrier)
-  const uint32_t t = s_tot[lane];
-  uint32_t incl = t;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-    if (lane >= d) incl += y;
-  }
-  const uint32_t n32 = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  const uint32_t offset = __shfl_sync(0xFFFFFFFFu, incl - t, warp);
-  const uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, s_lo[lane]);
-  const uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, s_hi[lane]);
-  const std::uint64_t n = n32;
-
-  std::uint16_t* lw = lut + base + lane;
-  if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
-    for (int r = 0; r < kRows; ++r) lw[r * 32] = static_cast<std::uint16_t>(base + r * 32 + lane);
-    if (threadIdx.x == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
-    return;
-  }
-  const std::uint64_t cdf_min = __ldg(hist + lo);
-  if (threadIdx.x == 0)
-    *stats = gpcx_lut_stats{n, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
-  const std::uint64_t d = n - cdf_min;
-  const double inv_d = d != 0 ? 1.0 / static_cast<double>(d) : 0.0;
-  const std::uint64_t span = hi - lo;
-  const double inv_span = span != 0 ? 1.0 / static_cast<double>(span) : 0.0;
-  std::uint64_t carry = offset;
-#pragma unroll 4
-  for (int r = 0; r < kRows; ++r) {
-    const uint32_t v = base + r * 32 + lane;
-    uint32_t x = __ldg(hw + r * 32);
-    uint32_t inc = x;
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, dd);
-      if (lane >= dd) inc += y;
-    }
-    uint32_t e;
-    if (mode == GPCX_LUT_STRETCH) {
-      if (span == 0) e = v;
-      else if (v <= lo) e = 0;
-      else if (v >= hi) e = 65535;
-      else e = static_cast<uint32_t>(udiv_exact((v - lo) * 65535ull + span / 2, span, inv_span));
-    } else {
-      e = equalize_entry(v, carry + inc, cdf_min, d, inv_d, lo);
-    }
-    lw[r * 32] = static_cast<std::uint16_t>(e);
-    carry += __shfl_sync(0xFFFFFFFFu, inc, 31);
-  }
-}
-
 // Fused histogram merge + LUT build, one cooperative grid of 128 CTAs x 256
 // threads (every CTA resident): thread t of CTA b owns bins 2w, 2w+1 with
 // w = 256b + t.
@@ -336,7 +249,6 @@ __global__ void __launch_bounds__(1024, 1)
 //   grid.sync
 //   phase 2  every CTA derives n, lo, hi and its cdf offset from the 128
 //            published triples, scans its 512 bins and writes its LUT slice.
-// Replaces merge_kernel + the single-CTA from_hist_kernel on the hot path.
 constexpr int kBuildCtas = kWords / 256;  // 128
 
 __global__ void __launch_bounds__(256)

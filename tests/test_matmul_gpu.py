@@ -172,15 +172,20 @@ def test_gpcx_run_matmul_f32(gpu):
     _check(payload.view(np.float32).reshape(m, n), A, B, O.PREC_F32)
 
 
-def test_gpcx_run_matmul_block_rows_invariant(gpu):
-    """Block-row sharding (device 0 bound 3x) gives the bitwise same C."""
-    m, k, n = 4096, 4096, 4096  # 1.4e11 flop: above the sharding threshold
-    A, B = _mats(O.MAT_UNIFORM32, 6, m, k, n)
+@pytest.mark.parametrize("prec,m,k,n", [("f32", 4096, 4096, 4096), ("bf16", 4100, 4097, 4104)])
+def test_gpcx_run_matmul_block_rows_invariant(gpu, prec, m, k, n):
+    """Block-row sharding (device 0 bound 3x; B staged in k-slices and
+    completed by peer copies) gives the bitwise same C."""
+    A, B = _mats(O.MAT_UNIFORM32, 6, m, k, n)  # >= 2^36 flop: above the sharding threshold
     payload_in = np.concatenate([A.ravel(), B.ravel()])
-    _, one = G.run("MATMUL", f"m={m},k={k},n={n}", payload_in)
+    params = f"m={m},k={k},n={n},prec={prec}"
+    _, one = G.run("MATMUL", params, payload_in)
     try:
         G.init([0, 0, 0])
-        _, three = G.run("MATMUL", f"m={m},k={k},n={n}", payload_in)
+        _, three = G.run("MATMUL", params, payload_in)
     finally:
         G.init([0])
     assert np.array_equal(one, three)
+    rows = np.arange(0, m, 397)
+    C = one.view(np.float32).reshape(m, n)
+    _check(C, A, B, O.PREC_F32 if prec == "f32" else O.PREC_BF16, rows=rows)

@@ -1,2 +1,2 @@
-timeout 1200 python bench.py --steps 10 --warmup 3 --workload c5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
-tail -c 600 gpurun_out/bench_c5.err
+set -x
+timeout 900 python -m pytest tests -x -q -m gpu -k "matmul" > gpurun_out/t_mm.log 2>&1; tail -5 gpurun_out/t_mm.log
