@@ -1,0 +1,133 @@
+// hist_probe.cu -- what bounds the shared-memory histogram on sm_100a?
+// (design exploration for lut.cu's hist_kernel; not product code)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/hist_probe tools/hist_probe.cu
+// Modes (each pixel = one count):
+//   0 red.shared, packed u16 pairs (the product's addressing)
+//   1 red.shared, address forced into bank == lane   (bank-conflict free)
+//   2 red.shared, every lane the same word            (address conflicts)
+//   3 half the pixels red.shared, half red.global into a per-CTA L2 histogram
+//   4 a quarter of the pixels to red.global
+//   5 all pixels red.global (per-CTA L2 histogram)
+//   6 __match_any_sync aggregation, one red.shared per distinct value
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void gen(uint16_t* out, uint64_t n, int kind, uint64_t cols) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t h = sm64(0x5eed ^ i);
+    if (kind) out[i] = h & 0xFFFF;
+    else { uint64_t r = i / cols, c = i % cols; long long v = 1024 + (3071ull * (r + c)) / (2 * cols - 2) + ((long long)(h >> 58) - 32); out[i] = v; }
+  }
+}
+
+__device__ __forceinline__ uint4 ldnc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void reds(uint32_t* bins, uint32_t w, uint32_t inc) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bins + w);
+  asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(addr), "r"(inc) : "memory");
+}
+__device__ __forceinline__ void redg(uint32_t* p, uint32_t inc) {
+  asm volatile("red.global.add.u32 [%0], %1;" :: "l"(p), "r"(inc) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh) {
+  extern __shared__ uint4 sm[];
+  uint32_t* bins = (uint32_t*)sm;
+  for (int i = threadIdx.x; i < 8192; i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* mine = gh + (uint64_t)blockIdx.x * 65536;
+  const uint4* body = (const uint4*)img;
+  const uint64_t nvec = n / 8, stride = (uint64_t)gridDim.x * 1024;
+  auto px = [&](uint32_t v, int slot) {
+    const uint32_t inc = 1u << ((v & 1) << 4);
+    if (MODE == 0) reds(bins, v >> 1, inc);
+    else if (MODE == 1) reds(bins, ((v >> 1) & ~31u) | lane, inc);
+    else if (MODE == 2) reds(bins, 7, inc);
+    else if (MODE == 3) { if (slot & 1) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
+    else if (MODE == 4) { if ((slot & 3) == 3) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
+    else if (MODE == 5) redg(mine + v, 1);
+    else if (MODE == 6) {
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, v);
+      if ((peers & ((1u << lane) - 1)) == 0) reds(bins, v >> 1, inc * __popc(peers));
+    }
+  };
+  auto vec = [&](uint4 q) {
+    px(q.x & 0xFFFF, 0); px(q.x >> 16, 1); px(q.y & 0xFFFF, 2); px(q.y >> 16, 3);
+    px(q.z & 0xFFFF, 4); px(q.z >> 16, 5); px(q.w & 0xFFFF, 6); px(q.w >> 16, 7);
+  };
+  uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = ldnc(body + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vec(q[u]);
+  }
+  for (; i < nvec; i += stride) vec(ldnc(body + i));
+  __syncthreads();
+  uint4* dst = (uint4*)(parts + (uint64_t)blockIdx.x * 32768);
+  for (int j = threadIdx.x; j < 8192; j += 1024) dst[j] = sm[j];
+}
+
+template <int MODE>
+void run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh, int sms) {
+  cudaFuncSetAttribute(hist<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 6; ++r) {
+    cudaMemsetAsync(gh, 0, (uint64_t)sms * 65536 * 4);
+    cudaEventRecord(a);
+    hist<MODE><<<sms, 1024, 131072>>>(img, n, parts, gh);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  cudaError_t e = cudaGetLastError();
+  printf("%-34s %8.4f ms  %7.1f GB/s  %6.2f px/clk/SM@1.9GHz %s\n", name, best, 2.0 * n / best / 1e6,
+         n / (best * 1e-3) / sms / 1.9e9, e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main() {
+  const uint64_t rows = 32768, cols = 32768, n = rows * cols;
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  uint16_t* img;
+  uint32_t *parts, *gh;
+  CK(cudaMalloc(&img, n * 2));
+  CK(cudaMalloc(&parts, 300ull * 131072));
+  CK(cudaMalloc(&gh, (uint64_t)sms * 65536 * 4));
+  for (int kind = 0; kind < 2; ++kind) {
+    gen<<<4096, 256>>>(img, n, kind, cols);
+    CK(cudaDeviceSynchronize());
+    printf("== %s\n", kind ? "uniform16" : "ramp12");
+    run<0>("0 red.shared packed", img, n, parts, gh, sms);
+    run<1>("1 red.shared bank==lane", img, n, parts, gh, sms);
+    run<2>("2 red.shared same word", img, n, parts, gh, sms);
+    run<3>("3 1/2 red.global", img, n, parts, gh, sms);
+    run<4>("4 1/4 red.global", img, n, parts, gh, sms);
+    run<5>("5 all red.global", img, n, parts, gh, sms);
+    run<6>("6 match_any aggregated", img, n, parts, gh, sms);
+  }
+  return 0;
+}
