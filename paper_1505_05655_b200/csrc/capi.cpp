@@ -283,9 +283,13 @@ int gpcx_lut_apply_device(const uint16_t* lut, const uint16_t* in, uint16_t* out
 int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n, int mode,
                             uint16_t* lut, gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
                             void* stream) {
-  const int rc = gpcx_lut_gen_device(in, n, mode, lut, stats, ws, ws_bytes, stream);
-  if (rc != GPCX_OK) return rc;
-  return gpcx_lut_apply_device(lut, in, out, n, stream);
+  return guarded([&] {
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    gpcx::lut::launch_correct(in, out, n, mode, lut, stats, ws, as_stream(stream));
+  });
 }
 
 int gpcx_matmul_workspace_size(int prec, uint64_t m, uint64_t n, uint64_t k, uint64_t* bytes) {

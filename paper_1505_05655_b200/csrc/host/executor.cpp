@@ -167,7 +167,10 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     auto* dimg = s.a.as<std::uint16_t>();
     if (flag != Flag::LutApply) {
       if (G == 1) {
-        if (equalize) {
+        if (equalize && need_apply) {  // one fused launch: histogram -> LUT -> apply
+          lut::launch_correct(dimg, dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr,
+                              s.stream);
+        } else if (equalize) {
           lut::launch_hist_lut(dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr, s.stream);
         } else {
           lut::launch_minmax(dimg, bn, s.d_stats(), s.lut_ws.ptr, s.stream);
@@ -186,7 +189,8 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
                                 cudaMemcpyDeviceToHost, s.stream));
     }
     if (need_apply) {
-      lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
+      if (!(G == 1 && equalize && flag != Flag::LutApply))  // else applied by the fused launch
+        lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
       rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
       if (lut_out != nullptr && i == 0)
         GPCX_CUDA(cudaMemcpy(lut_out, s.d_lut(), task::kLutBytes, cudaMemcpyDeviceToHost));

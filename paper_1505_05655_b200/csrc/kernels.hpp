@@ -36,10 +36,14 @@ void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
 // LUT workspace, used for the per-CTA scan triples).
 void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
                       gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
-// Single-device LUT_GEN equalize/stretch-from-histogram: hist_kernel + the
-// fused merge/build kernel (the histogram lands in ws_hist(ws)).
+// Single-device LUT_GEN equalize: one cooperative fused_kernel launch
+// (the histogram lands in ws_hist(ws)).
 void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+// Single-device LUT_CORRECT (LUT_GEN + apply; in == out allowed): equalize
+// with co-aligned buffers is ONE fused_kernel launch; otherwise gen + apply.
+void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
+                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 void launch_minmax(const std::uint16_t* img, std::uint64_t n,
                    gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 void launch_from_minmax(const gpcx_lut_stats* stats, std::uint16_t* lut,

@@ -6,11 +6,14 @@
 // bit-identical to oracle/gpcx_oracle.c and independent of the CTA count /
 // GPU count (the parexec invariance contract, proj/include/gpc/parexec.hpp:11-31).
 //
-// Kernels (all HBM-bound; see DESIGN.md for the roofline of each):
+// Kernels (see DESIGN.md for the roofline of each):
+//   fused_kernel    single-device equalize LUT_GEN / LUT_CORRECT in one
+//                   cooperative launch: histogram -> merge -> LUT [-> apply].
 //   hist_kernel     persistent, 1 CTA/SM, 128 KiB smem histogram of packed
 //                   u16 pairs, 128-bit streaming loads.   2 B/px read.
+//                   (multi-GPU: local histogram before the all-reduce)
 //   merge_kernel    column-sum of the per-CTA partials (+ overflow fixups).
-//   from_hist       1 CTA: block scan -> equalize LUT.
+//   build_kernel    cooperative LUT build from a (all-reduced) histogram.
 //   minmax_kernel   warp-shuffle (redux) min/max for stretch.  2 B/px read.
 //   from_minmax     stretch LUT.
 //   apply_kernel    persistent, LUT staged in 128 KiB smem, 128-bit
@@ -49,7 +52,7 @@ constexpr int kThreads = 1024;
 constexpr std::uint64_t kOverflowOff = 0;
 constexpr std::uint64_t kHistOff = 256 * 1024;
 constexpr std::uint64_t kMinMaxOff = 512 * 1024;
-constexpr std::uint64_t kBlocksOff = kMinMaxOff + 4 * 1024;  // build_kernel's 128 triples
+constexpr std::uint64_t kBlocksOff = kMinMaxOff + 4 * 1024;  // 128 slice summaries (2 KiB)
 constexpr std::uint64_t kPartsOff = kMinMaxOff + 8 * 1024;
 constexpr int kSmemHist = kWords * 4;  // 128 KiB
 constexpr int kSmemLut = kBins * 2;    // 128 KiB
@@ -117,6 +120,95 @@ __device__ __host__ __forceinline__ std::uint64_t head_len(const void* p,
   return h < n ? h : n;
 }
 
+__device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
+  uint4 r;
+  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.x >> 16]) << 16);
+  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.y >> 16]) << 16);
+  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.z >> 16]) << 16);
+  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.w >> 16]) << 16);
+  return r;
+}
+
+// Histogram of img[0, n) into the packed smem bins; CTA `cta` of `ctas`
+// (grid-stride over 128-bit vectors, two-vector software pipeline: the next
+// stage's loads are in flight while this stage's 16 samples are counted).
+__device__ __forceinline__ void count_image(const std::uint16_t* img,
+                                            std::uint64_t n, int cta, int ctas,
+                                            uint32_t* bins, uint32_t* overflow) {
+  const std::uint64_t head = head_len(img, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  if (cta == 0)
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one(bins, overflow, img[i]);
+  if (cta == ctas - 1)
+    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
+      count_one(bins, overflow, img[i]);
+  const uint4* body = reinterpret_cast<const uint4*>(img + head);
+  const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
+  std::uint64_t i = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
+  uint4 q[2], nq[2];
+  bool have = i + stride < nvec;
+  if (have) {
+    q[0] = ld_stream(body + i);
+    q[1] = ld_stream(body + i + stride);
+  }
+  while (have) {
+    const std::uint64_t nx = i + 2 * stride;
+    const bool nhave = nx + stride < nvec;
+    if (nhave) {
+      nq[0] = ld_stream(body + nx);
+      nq[1] = ld_stream(body + nx + stride);
+    }
+    count_vec(bins, overflow, q[0]);
+    count_vec(bins, overflow, q[1]);
+    q[0] = nq[0];
+    q[1] = nq[1];
+    i = nx;
+    have = nhave;
+  }
+  for (; i < nvec; i += stride) count_vec(bins, overflow, ld_stream(body + i));
+}
+
+// out = LUT[in] over [0, n) with the LUT in smem; CTA `cta` of `ctas`.
+// Two vectors per stage, the next stage's loads in flight while this one is
+// looked up and stored (tools/apply_bench.cu: = cudaMemcpy D2D bandwidth).
+__device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const std::uint16_t* in,
+                                            std::uint16_t* out, std::uint64_t n, int cta,
+                                            int ctas) {
+  const std::uint64_t tid = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
+  const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
+  const std::uint64_t head = head_len(in, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  if (tid < head) out[tid] = s_lut[in[tid]];
+  if (tid < n - tail0) out[tail0 + tid] = s_lut[in[tail0 + tid]];
+  const uint4* src = reinterpret_cast<const uint4*>(in + head);
+  uint4* dst = reinterpret_cast<uint4*>(out + head);
+  constexpr int kU = 2;
+  std::uint64_t i = tid;
+  uint4 q[kU], nq[kU];
+  bool have = i + (kU - 1) * stride < nvec;
+  if (have) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) q[u] = ld_stream(src + i + u * stride);
+  }
+  while (have) {
+    const std::uint64_t nx = i + kU * stride;
+    const bool nhave = nx + (kU - 1) * stride < nvec;
+    if (nhave) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) nq[u] = ld_stream(src + nx + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
+#pragma unroll
+    for (int u = 0; u < kU; ++u) q[u] = nq[u];
+    i = nx;
+    have = nhave;
+  }
+  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     hist_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
                 uint32_t* __restrict__ parts,
@@ -127,47 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     smem_u4[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
-  const std::uint64_t head = head_len(img, n);
-  const std::uint64_t nvec = (n - head) >> 3;
-  const std::uint64_t tail0 = head + (nvec << 3);
-  if (blockIdx.x == 0) {
-    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads)
-      count_one(bins, overflow, img[i]);
-  }
-  if (blockIdx.x == gridDim.x - 1) {
-    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
-      count_one(bins, overflow, img[i]);
-  }
-
-  const uint4* body = reinterpret_cast<const uint4*>(img + head);
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
-  std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
-  // Two-vector software pipeline: the next stage's loads are in flight while
-  // this stage's 16 samples are counted (tools/hist_bench.cu: 5% faster than
-  // load-then-count; the smem atomic rate is the remaining bound).
-  {
-    uint4 q[2], nq[2];
-    bool have = i + stride < nvec;
-    if (have) {
-      q[0] = ld_stream(body + i);
-      q[1] = ld_stream(body + i + stride);
-    }
-    while (have) {
-      const std::uint64_t nx = i + 2 * stride;
-      const bool nhave = nx + stride < nvec;
-      if (nhave) {
-        nq[0] = ld_stream(body + nx);
-        nq[1] = ld_stream(body + nx + stride);
-      }
-      count_vec(bins, overflow, q[0]);
-      count_vec(bins, overflow, q[1]);
-      q[0] = nq[0];
-      q[1] = nq[1];
-      i = nx;
-      have = nhave;
-    }
-  }
-  for (; i < nvec; i += stride) count_vec(bins, overflow, ld_stream(body + i));
+  count_image(img, n, blockIdx.x, gridDim.x, bins, overflow);
   __syncthreads();
 
   uint4* dst = reinterpret_cast<uint4*>(parts + static_cast<std::uint64_t>(blockIdx.x) * kWords);
@@ -354,6 +406,217 @@ __global__ void __launch_bounds__(256)
   reinterpret_cast<uint32_t*>(lut)[w] = e0 | (e1 << 16);
 }
 
+#ifdef GPCX_LUT_TRACE
+// Phase timestamps for tools/fused_trace.cu (compiled out of the library).
+__device__ unsigned long long* g_lut_trace;
+#define LUT_STAMP(k)                                                          \
+  do {                                                                        \
+    if (threadIdx.x == 0) {                                                   \
+      unsigned long long ts_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));                 \
+      g_lut_trace[blockIdx.x * 16 + (k)] = ts_;                               \
+    }                                                                         \
+  } while (0)
+#else
+#define LUT_STAMP(k) do {} while (0)
+#endif
+
+// The whole single-device equalize LUT_GEN / LUT_CORRECT in ONE cooperative
+// launch, 1 CTA x 1024 threads per SM (every CTA resident):
+//   phase 1  CTAs < nparts count their share of the image into packed smem
+//            bins and flush them as partials;                      grid.sync
+//   phase 2  CTA b < 128 owns bins [512b, 512b + 512): 16 groups of 64
+//            threads column-sum 1/16 of the partials each with 128-bit
+//            loads (16x the memory-level parallelism of one thread per
+//            word), a smem reduction joins the groups, + overflow (zeroed
+//            for the next call); publishes the CTA's total / first / last
+//            non-empty bin;                                        grid.sync
+//   phase 3  each of those CTAs derives n, lo, hi and its cdf offset from the
+//            128 triples and writes its 512 LUT entries;  [apply:] grid.sync
+//   phase 4  every CTA stages the LUT in smem (over the dead bins) and maps
+//            the image -- which, at C1 size, phase 1 left in L2.
+// Replaces hist_kernel + build_kernel (+ apply_kernel): no launch gaps, and
+// the partial merge is no longer latency-bound (~17 us -> a few us).
+constexpr int kSlices = kWords / 256;    // 128 CTAs own 512 bins in phases 2-3
+constexpr int kGroups = kThreads / 64;   // partial groups per slice
+static_assert(kGroups * 512 * 4 <= kWords * 4, "phase-2 reduction fits in the bins");
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_kernel(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int nparts,
+                 uint32_t* __restrict__ parts, uint32_t* __restrict__ overflow,
+                 uint32_t* __restrict__ hist, uint4* __restrict__ blocks, int mode,
+                 std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
+                 int apply) {
+  extern __shared__ uint4 smem_u4[];
+  uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
+  __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8], s_wfcount[8];
+  cg::grid_group grid = cg::this_grid();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+  LUT_STAMP(0);
+  // ---- phase 1: per-CTA histograms
+  if (static_cast<int>(blockIdx.x) < nparts) {
+    for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    count_image(img, n, blockIdx.x, nparts, bins, overflow);
+    __syncthreads();
+    LUT_STAMP(1);
+    uint4* dst = reinterpret_cast<uint4*>(parts + static_cast<std::uint64_t>(blockIdx.x) * kWords);
+    for (int j = t; j < kWords / 4; j += kThreads) dst[j] = smem_u4[j];
+  }
+  LUT_STAMP(2);
+  grid.sync();
+  LUT_STAMP(3);
+
+  // ---- phase 2: merge this CTA's 512-bin slice
+  const bool slice_cta = static_cast<int>(blockIdx.x) < kSlices;
+  const int w = blockIdx.x * 256 + t;  // word (bins 2w, 2w+1) of threads t < 256
+  uint32_t c0 = 0, c1 = 0, inc = 0;
+  if (slice_cta) {
+    const int quad = t & 63, group = t >> 6;
+    const uint4* pq = reinterpret_cast<const uint4*>(parts) + blockIdx.x * 64 + quad;
+    constexpr std::uint64_t kPartQuads = kWords / 4;
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto add = [&](uint4 x) {
+      acc[0] += x.x & 0xFFFFu; acc[1] += x.x >> 16;
+      acc[2] += x.y & 0xFFFFu; acc[3] += x.y >> 16;
+      acc[4] += x.z & 0xFFFFu; acc[5] += x.z >> 16;
+      acc[6] += x.w & 0xFFFFu; acc[7] += x.w >> 16;
+    };
+    int p = group;
+    for (; p + 7 * kGroups < nparts; p += 8 * kGroups) {  // 8 loads in flight
+      uint4 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(pq + (p + u * kGroups) * kPartQuads);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) add(x[u]);
+    }
+    for (; p < nparts; p += kGroups) add(__ldcg(pq + p * kPartQuads));
+    // red[group][bin], bin = 8 * quad + j of the slice
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
+    __syncthreads();
+    if (t < 256) {
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        lo += bins[g * 512 + 2 * t];
+        hi += bins[g * 512 + 2 * t + 1];
+      }
+      const uint2 ov = __ldcg(reinterpret_cast<const uint2*>(overflow) + w);
+      reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
+      c0 = lo + ov.x;
+      c1 = hi + ov.y;
+      reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
+      inc = c0 + c1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const uint32_t first = c0 ? 2u * w : (c1 ? 2u * w + 1 : 0xFFFFFFFFu);
+      const uint32_t last = c1 ? 2u * w + 1 : (c0 ? 2u * w : 0u);
+      const uint32_t wfirst = __reduce_min_sync(0xFFFFFFFFu, first);
+      const uint32_t wlast = __reduce_max_sync(0xFFFFFFFFu, last);
+      // count of the first non-empty bin (cdf_min if it is the global one)
+      const uint32_t wfcount = __reduce_add_sync(
+          0xFFFFFFFFu, first == wfirst && first != 0xFFFFFFFFu ? (c0 ? c0 : c1) : 0u);
+      if (lane == 31) s_wsum[warp] = inc;
+      if (lane == 0) {
+        s_wfirst[warp] = wfirst;
+        s_wlast[warp] = wlast;
+        s_wfcount[warp] = wfcount;
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      uint32_t sum = 0, first = 0xFFFFFFFFu, last = 0, fcount = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        sum += s_wsum[i];
+        if (s_wfirst[i] < first) {
+          first = s_wfirst[i];
+          fcount = s_wfcount[i];
+        }
+        last = max(last, s_wlast[i]);
+      }
+      // (total, first, last, count(first)): phase 3 needs no second load
+      blocks[blockIdx.x] = make_uint4(sum, first, last, fcount);
+    }
+  }
+  LUT_STAMP(4);
+  grid.sync();
+  LUT_STAMP(5);
+
+  // ---- phase 3: LUT slice
+  if (slice_cta && t < 256) {
+    uint32_t n32 = 0, off = 0, lo = 0xFFFFFFFFu, hi = 0, lo_count = 0;
+    static_assert(kSlices % 32 == 0, "whole warps of slice triples");
+#pragma unroll
+    for (int b0 = 0; b0 < kSlices; b0 += 32) {
+      const int b = b0 + lane;
+      const uint4 q = __ldcg(blocks + b);
+      n32 += q.x;
+      if (b < static_cast<int>(blockIdx.x)) off += q.x;
+      if (q.y < lo) {  // slices are disjoint: each first bin is distinct
+        lo = q.y;
+        lo_count = q.w;
+      }
+      if (q.x != 0) hi = max(hi, q.z);
+    }
+    n32 = __reduce_add_sync(0xFFFFFFFFu, n32);
+    off = __reduce_add_sync(0xFFFFFFFFu, off);
+    const uint32_t my_lo = lo;
+    lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+    hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    const uint32_t cdf_min32 = __reduce_add_sync(0xFFFFFFFFu, my_lo == lo ? lo_count : 0u);
+    uint32_t warp_off = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < warp) warp_off += s_wsum[i];
+    const uint32_t v0 = 2u * w;
+    uint32_t e0, e1;
+    if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
+      e0 = v0;
+      e1 = v0 + 1;
+      if (w == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
+    } else {
+      const std::uint64_t nn = n32;
+      const std::uint64_t cdf_min = cdf_min32;
+      if (w == 0) *stats = gpcx_lut_stats{nn, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
+      if (mode == GPCX_LUT_STRETCH) {
+        e0 = stretch_entry(v0, nn, lo, hi);
+        e1 = stretch_entry(v0 + 1, nn, lo, hi);
+      } else {
+        const std::uint64_t d = nn - cdf_min;
+        const double inv_d = d != 0 ? 1.0 / static_cast<double>(d) : 0.0;
+        const std::uint64_t cdf1 = static_cast<std::uint64_t>(off) + warp_off + inc;
+        e0 = equalize_entry(v0, cdf1 - c1, cdf_min, d, inv_d, lo);
+        e1 = equalize_entry(v0 + 1, cdf1, cdf_min, d, inv_d, lo);
+      }
+    }
+    reinterpret_cast<uint32_t*>(lut)[w] = e0 | (e1 << 16);
+  }
+  LUT_STAMP(6);
+  if (!apply) return;
+  grid.sync();
+  LUT_STAMP(7);
+
+  // ---- phase 4: apply
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(lut);
+    for (int i = t; i < kBins / 8; i += kThreads) smem_u4[i] = __ldcg(src + i);
+  }
+  __syncthreads();
+  LUT_STAMP(8);
+  apply_image(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
+              gridDim.x);
+#ifdef GPCX_LUT_TRACE
+  __syncthreads();
+#endif
+  LUT_STAMP(9);
+}
+
 __device__ __forceinline__ void minmax_vec(uint4 q, uint32_t& mn2,
                                            uint32_t& mx2) {
   mn2 = __vminu2(mn2, __vminu2(__vminu2(q.x, q.y), __vminu2(q.z, q.w)));
@@ -458,15 +721,6 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-__device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
-  uint4 r;
-  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.x >> 16]) << 16);
-  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.y >> 16]) << 16);
-  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.z >> 16]) << 16);
-  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.w >> 16]) << 16);
-  return r;
-}
-
 // out = LUT[in].  The 128 KiB LUT is staged once per CTA in shared memory
 // (1 CTA/SM, persistent grid); the image streams through with 128-bit
 // loads/stores, kUnroll vectors in flight per thread.
@@ -481,48 +735,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
-  const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
-
   if (!vector_ok) {  // mismatched alignment of in/out: scalar path
-    for (std::uint64_t i = tid; i < n; i += stride) out[i] = s_lut[in[i]];
+    const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    for (std::uint64_t i = tid; i < n; i += static_cast<std::uint64_t>(gridDim.x) * kThreads)
+      out[i] = s_lut[in[i]];
     return;
   }
-  const std::uint64_t head = head_len(in, n);
-  const std::uint64_t nvec = (n - head) >> 3;
-  const std::uint64_t tail0 = head + (nvec << 3);
-  if (tid < head) out[tid] = s_lut[in[tid]];
-  if (tid < n - tail0) out[tail0 + tid] = s_lut[in[tail0 + tid]];
-
-  const uint4* src = reinterpret_cast<const uint4*>(in + head);
-  uint4* dst = reinterpret_cast<uint4*>(out + head);
-  // Software pipeline, two vectors per stage: the loads of stage g+1 are in
-  // flight while stage g is looked up and stored, so the smem gathers never
-  // leave the memory system without requests (tools/apply_bench.cu: 6.48
-  // TB/s, = cudaMemcpy D2D, vs 5.6-5.9 TB/s for the load-then-use loop).
-  constexpr int kU = 2;
-  std::uint64_t i = tid;
-  uint4 q[kU], nq[kU];
-  bool have = i + (kU - 1) * stride < nvec;
-  if (have) {
-#pragma unroll
-    for (int u = 0; u < kU; ++u) q[u] = ld_stream(src + i + u * stride);
-  }
-  while (have) {
-    const std::uint64_t nx = i + kU * stride;
-    const bool nhave = nx + (kU - 1) * stride < nvec;
-    if (nhave) {
-#pragma unroll
-      for (int u = 0; u < kU; ++u) nq[u] = ld_stream(src + nx + u * stride);
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
-#pragma unroll
-    for (int u = 0; u < kU; ++u) q[u] = nq[u];
-    i = nx;
-    have = nhave;
-  }
-  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
+  apply_image(s_lut, in, out, n, blockIdx.x, gridDim.x);
 }
 
 bool g_attrs_set[64] = {};
@@ -586,17 +805,55 @@ void launch_from_hist(const uint32_t* hist, int mode, std::uint16_t* lut,
                stream);
 }
 
-void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
-                     gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
-  set_attrs_once();
+namespace {
+// fused_kernel over the whole device; `out` == nullptr -> LUT_GEN only.
+void launch_fused(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int mode,
+                  std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  GPCX_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64 || !attr_set[dev]) {
+    GPCX_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemHist));
+    if (dev < 64) attr_set[dev] = true;
+  }
   auto* base = static_cast<unsigned char*>(ws);
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
   auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
   auto* hist = reinterpret_cast<uint32_t*>(base + kHistOff);
-  const int p = parts_for(n, device_sm_count());
-  hist_kernel<<<p, kThreads, kSmemHist, stream>>>(img, n, parts, overflow);
-  GPCX_LAUNCH_CHECK();
-  launch_build(parts, p, overflow, hist, 1, mode, ws, lut, stats, stream);
+  auto* blocks = reinterpret_cast<uint4*>(base + kBlocksOff);
+  const int sms = device_sm_count();
+  int nparts = parts_for(n, sms);
+  int apply = out != nullptr;
+  std::uint16_t* dst = out;
+  void* args[] = {const_cast<std::uint16_t**>(&img), &dst, &n, &nparts, &parts, &overflow,
+                  &hist, &blocks, &mode, &lut, &stats, &apply};
+  GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fused_kernel),
+                                        dim3(std::max(sms, kSlices)), dim3(kThreads), args,
+                                        kSmemHist, stream));
+}
+}  // namespace
+
+void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
+                     gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  launch_fused(img, nullptr, n, mode, lut, stats, ws, stream);
+}
+
+void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
+                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  const bool vector_ok =
+      ((reinterpret_cast<std::uintptr_t>(in) ^ reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
+  if (mode == GPCX_LUT_EQUALIZE && vector_ok && n != 0) {
+    launch_fused(in, out, n, mode, lut, stats, ws, stream);
+    return;
+  }
+  if (mode == GPCX_LUT_EQUALIZE) {
+    launch_fused(in, nullptr, n, mode, lut, stats, ws, stream);
+  } else {
+    launch_minmax(in, n, stats, ws, stream);
+    launch_from_minmax(stats, lut, stream);
+  }
+  launch_apply(lut, in, out, n, stream);
 }
 
 void launch_minmax(const std::uint16_t* img, std::uint64_t n,

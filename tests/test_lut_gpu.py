@@ -118,6 +118,46 @@ def test_apply_unaligned_and_inplace(gpu, in_off, out_off):
     assert np.array_equal(u16(inplace), lut_np[u16(src)])
 
 
+@pytest.mark.parametrize("in_off,out_off", [(0, 0), (1, 1), (3, 3), (1, 0), (0, 5), (None, None)])
+def test_lut_correct_fused_alignment_and_inplace(gpu, in_off, out_off):
+    """LUT_CORRECT equalize is one cooperative launch when in/out are
+    co-aligned (incl. in place), the gen + apply pair otherwise: same bytes."""
+    torch, D = _dev()
+    n = 1_000_003
+    base = D.synth_image(O.IMG_RAMP12, 9, 1, n + 16)
+    if in_off is None:  # in place
+        src = base[3:3 + n].clone()
+        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), O.LUT_EQUALIZE)
+        dst = src
+    else:
+        src = base[in_off:in_off + n]
+        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), O.LUT_EQUALIZE)
+        dst = torch.zeros(n + 16, dtype=torch.int16, device=gpu)[out_off:out_off + n]
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    D.lut_correct(src, dst, O.LUT_EQUALIZE, lut, stats, ws)
+    assert np.array_equal(u16(dst), ref_out)
+    assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
+
+
+def test_lut_correct_fused_counter_wraps_and_reuse(gpu):
+    """Packed-counter wraps through the fused path, twice on one workspace
+    (the overflow counters must come back zeroed)."""
+    torch, D = _dev()
+    n = 3_000_000
+    vals = np.empty(n, dtype=np.uint16)
+    vals[0::3] = 1000
+    vals[1::3] = 1001
+    vals[2::3] = 77
+    img = torch.from_numpy(vals.view(np.int16)).to(gpu)
+    ref_out, ref_lut, ref_st = O.lut_correct(vals, O.LUT_EQUALIZE)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    for _ in range(2):
+        out = torch.empty_like(img)
+        D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+        assert np.array_equal(u16(out), ref_out) and np.array_equal(u16(lut), ref_lut)
+        assert D.read_stats(stats) == ref_st
+
+
 def test_constant_and_two_level_images(gpu):
     torch, D = _dev()
     for vals in ([1234] * 1000, [300] * 700 + [40000] * 333, [0] * 10 + [65535] * 10):

@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--rows", type=int, default=32768)
     ap.add_argument("--cols", type=int, default=32768)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--flush", action="store_true",
+                    help="write 512 MiB between reps so every rep starts with a cold L2")
     args = ap.parse_args()
     import torch
     from paper_1505_05655_b200 import device as D
@@ -27,6 +29,7 @@ def main():
     hist = torch.zeros(65536, dtype=torch.int32, device="cuda")
     lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
     out = torch.empty(n, dtype=torch.int16, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if args.flush else None
     res = {}
     for kind, name in ((0, "ramp12"), (1, "uniform16")):
         img = D.synth_image(kind, 0x5EED, args.rows, args.cols)
@@ -36,17 +39,21 @@ def main():
             "hist+merge": lambda: D.lut_hist(img, hist, ws),
             "from_hist": lambda: D.lut_from_hist(hist, 0, lut, stats, ws),
             "gen(hist+fused build)": lambda: D.lut_gen(img, 0, lut, stats, ws),
-            "correct(gen+apply)": lambda: D.lut_correct(img, out, 0, lut, stats, ws),
+            "correct(fused)": lambda: D.lut_correct(img, out, 0, lut, stats, ws),
+            "gen+apply(2 launches)": lambda: (D.lut_gen(img, 0, lut, stats, ws),
+                                              D.lut_apply(lut, img, out)),
             "minmax": lambda: D.lut_minmax(img, stats, ws),
             "apply": lambda: D.lut_apply(lut, img, out),
             "copy(torch)": lambda: out.copy_(img),
         }
         bytes_per = {"hist+merge": 2 * n, "from_hist": 0, "minmax": 2 * n, "apply": 4 * n,
                      "copy(torch)": 4 * n, "gen(hist+fused build)": 2 * n,
-                     "correct(gen+apply)": 6 * n}
+                     "correct(fused)": 6 * n, "gen+apply(2 launches)": 6 * n}
         for op, fn in ops.items():
             ts = []
-            for _ in range(args.reps + 2):
+            for i in range(args.reps + 2):
+                if flush is not None:
+                    flush.fill_(i & 0xFF)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
                 fn()

@@ -20,6 +20,13 @@ def main():
     args = ap.parse_args()
     import torch
     from paper_1505_05655_b200 import device as D
+    if "c1" in args.what:  # config C1: one 4096^2 LUT_CORRECT (fused_kernel)
+        img = D.synth_image(0, 0x5EED, 4096, 4096)
+        out = torch.empty_like(img)
+        lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(img.numel())
+        D.lut_correct(img, out, 0, lut, stats, ws)
+        torch.cuda.synchronize()
+        del img, out
     if "lut" in args.what:
         n = 32768 * 32768
         img = D.synth_image(0, 0x5EED, 32768, 32768)
