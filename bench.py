@@ -219,16 +219,17 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
             if record:
                 ev["h1"].append(E()); ev["h1"][-1].record(stream)
             return
-        # N GPUs: local histogram, NCCL all-reduce, identical LUT everywhere
+        # N GPUs: local histogram (fused_kernel, count stage), NCCL all-reduce
+        # of the 256 KiB histogram, then LUT + apply of the band (one launch)
         D.lut_hist(img, hist, ws, stream)
-        d.all_reduce_(hist)
-        D.lut_from_hist(hist, mode, lut, stats, ws, stream)
         if record:
-            ev["h1"].append(E()); ev["h1"][-1].record(stream)
             ev["a0"].append(E()); ev["a0"][-1].record(stream)
-        D.lut_apply(lut, img, out, stream)
+        d.all_reduce_(hist)
         if record:
             ev["a1"].append(E()); ev["a1"][-1].record(stream)
+        D.lut_correct_from_hist(hist, mode, img, out, lut, stats, ws, stream)
+        if record:
+            ev["h1"].append(E()); ev["h1"][-1].record(stream)
 
     for _ in range(warmup):
         step(False)
@@ -246,13 +247,14 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     hist_ms = sum(a.elapsed_time(b) for a, b in zip(ev["h0"], ev["h1"])) / steps
-    apply_ms = (sum(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"])) / steps
-                if ev["a0"] else None)
+    # N>1: time spent in the histogram all-reduce (between the two launches)
+    exch_ms = (sum(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"])) / steps
+               if ev["a0"] else None)
     # correctness guard on the measured buffers (device digest vs nothing
     # here; the oracle check of this exact band runs in the cpu leg).
     dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
     st = D.read_stats(stats)
-    return {"ms": ms, "hist_ms": hist_ms, "apply_ms": apply_ms, "band_px": n, "digest": dig,
+    return {"ms": ms, "hist_ms": hist_ms, "exch_ms": exch_ms, "band_px": n, "digest": dig,
             "stats": st, "clocks": clk.summary()}
 
 
@@ -525,7 +527,7 @@ def run_b200(args) -> None:
     mode = 0
     lut = lut_device_leg(d, args.steps, args.warmup, mode)
     ms = d.max(lut["ms"])
-    apply_ms = d.max(lut["apply_ms"]) if lut["apply_ms"] is not None else None
+    exch_ms = d.max(lut["exch_ms"]) if lut["exch_ms"] is not None else None
     hist_ms = d.max(lut["hist_ms"])
     mm = c4 = None
     if args.workload in ("all", "matmul"):
@@ -545,36 +547,23 @@ def run_b200(args) -> None:
     band_px = lut["band_px"]
     tr = traffic_from_profiles()
     step_ach = 6.0 * band_px / (ms / args.steps / 1e3) / 1e9
-    if apply_ms is None:
-        # one GPU: the step is ONE fused_kernel launch (histogram -> LUT ->
-        # apply); its algorithmic bytes are the step's 6 B/px.
-        fused_ach = 6.0 * band_px / (hist_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "lut::fused_kernel", "achieved": round(fused_ach, 1),
-                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(fused_ach / pk["hbm_gbs"], 4),
-                "traffic": tr.get("fused_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
-                "algorithmic_bytes_per_launch": 6 * band_px, "peak_source": pk["source"],
-                "kernels": {"fused_kernel": {"ms": round(hist_ms, 4),
-                                             "phases": "histogram (2 B/px, smem-atomic bound) | "
-                                                       "merge + LUT | apply (4 B/px)"},
-                            "step": {"achieved": round(step_ach, 1),
-                                     "frac": round(step_ach / pk["hbm_gbs"], 4),
-                                     "algorithmic_bytes": 6 * band_px}}}
-        launches = 1
-    else:
-        apply_ach = 4.0 * band_px / (apply_ms / 1e3) / 1e9
-        hist_ach = 2.0 * band_px / (hist_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "lut::apply_kernel", "achieved": round(apply_ach, 1),
-                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(apply_ach / pk["hbm_gbs"], 4),
-                "traffic": tr.get("apply_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
-                "algorithmic_bytes_per_launch": 4 * band_px, "peak_source": pk["source"],
-                "kernels": {"lut_gen (hist_kernel + merge_kernel + all-reduce + build_kernel)": {
-                                "achieved": round(hist_ach, 1), "frac": round(hist_ach / pk["hbm_gbs"], 4),
-                                "algorithmic_bytes": 2 * band_px, "ms": round(hist_ms, 4)},
-                            "apply_kernel": {"ms": round(apply_ms, 4)},
-                            "step": {"achieved": round(step_ach, 1),
-                                     "frac": round(step_ach / pk["hbm_gbs"], 4),
-                                     "algorithmic_bytes": 6 * band_px}}}
-        launches = 4
+    # fused_kernel launches (1 at N=1; count, then build+apply around the
+    # NCCL all-reduce at N>1) carry the step's 6 B/px of algorithmic traffic.
+    kern_ms = hist_ms - (exch_ms or 0.0)
+    fused_ach = 6.0 * band_px / (kern_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "lut::fused_kernel", "achieved": round(fused_ach, 1),
+            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(fused_ach / pk["hbm_gbs"], 4),
+            "traffic": tr.get("fused_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
+            "algorithmic_bytes_per_launch": 6 * band_px, "peak_source": pk["source"],
+            "kernels": {"fused_kernel": {"ms": round(kern_ms, 4),
+                                         "phases": "histogram (2 B/px, smem-atomic bound) | "
+                                                   "merge + LUT | apply (4 B/px)"},
+                        "step": {"achieved": round(step_ach, 1),
+                                 "frac": round(step_ach / pk["hbm_gbs"], 4),
+                                 "algorithmic_bytes": 6 * band_px}}}
+    if exch_ms is not None:
+        roof["kernels"]["histogram_all_reduce"] = {"ms": round(exch_ms, 4), "bytes": 262144}
+    launches = 1 if exch_ms is None else 2
     line = {"metric": METRIC, "value": round(value, 2), "unit": "Gpixel/s", "n_gpus": d.n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
@@ -583,7 +572,7 @@ def run_b200(args) -> None:
                        "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
                        "parallelism": f"row-band x{d.n}, NCCL all-reduce of the 65536-bin histogram",
                        "l2": "inputs larger than L2 (2 GiB scene)"},
-            # per step: fused_kernel at N=1; hist + merge + build + apply at N>1
+            # per step: fused_kernel once at N=1; count + build/apply launches at N>1
             "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": lut["clocks"]}
     e2e_steps = max(4, min(args.steps, 8))

@@ -177,10 +177,18 @@ int gpcx_lut_workspace_size(uint64_t n, uint64_t* bytes);
 int gpcx_lut_hist_device(const uint16_t* img, uint64_t n, uint32_t* hist,
                          void* ws, uint64_t ws_bytes, void* stream);
 /* LUT (65536 x u16) + stats from a histogram (stats: device pointer); ws is
- * a LUT workspace (scratch for the cooperative build kernel). */
+ * a LUT workspace (scratch for the per-slice scan summaries). */
 int gpcx_lut_from_hist_device(const uint32_t* hist, int mode, uint16_t* lut,
                               gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
                               void* stream);
+/* The second half of a row-band sharded LUT_CORRECT: LUT + stats from the
+ * merged (all-reduced) histogram, then out = LUT[in] over this band -- one
+ * kernel launch when in/out are 16-byte co-aligned (in == out allowed). */
+int gpcx_lut_correct_from_hist_device(const uint32_t* hist, int mode,
+                                      const uint16_t* in, uint16_t* out,
+                                      uint64_t n, uint16_t* lut,
+                                      gpcx_lut_stats* stats, void* ws,
+                                      uint64_t ws_bytes, void* stream);
 /* min/max statistics only (stretch mode's reduction); stats device ptr. */
 int gpcx_lut_minmax_device(const uint16_t* img, uint64_t n,
                            gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,

@@ -36,6 +36,7 @@ EXPORTS = [
     "gpcx_required_params", "gpcx_flags", "gpcx_run", "gpcx_lut_host", "gpcx_matmul_host",
     "gpcx_pinned_alloc", "gpcx_pinned_free",
     "gpcx_lut_workspace_size", "gpcx_lut_hist_device", "gpcx_lut_from_hist_device",
+    "gpcx_lut_correct_from_hist_device",
     "gpcx_lut_minmax_device", "gpcx_lut_from_minmax_device", "gpcx_lut_gen_device",
     "gpcx_lut_apply_device", "gpcx_lut_correct_device", "gpcx_matmul_workspace_size",
     "gpcx_matmul_device", "gpcx_synth_image_device", "gpcx_synth_matrix_device",
@@ -96,6 +97,7 @@ def _load() -> C.CDLL:
         "gpcx_lut_workspace_size": ([u64, pu64], i32),
         "gpcx_lut_hist_device": ([vp, u64, vp, vp, u64, vp], i32),
         "gpcx_lut_from_hist_device": ([vp, i32, vp, vp, vp, u64, vp], i32),
+        "gpcx_lut_correct_from_hist_device": ([vp, i32, vp, vp, u64, vp, vp, vp, u64, vp], i32),
         "gpcx_lut_minmax_device": ([vp, u64, vp, vp, u64, vp], i32),
         "gpcx_lut_from_minmax_device": ([vp, vp, vp], i32),
         "gpcx_lut_gen_device": ([vp, u64, i32, vp, vp, vp, u64, vp], i32),

@@ -245,6 +245,20 @@ int gpcx_lut_from_hist_device(const uint32_t* hist, int mode, uint16_t* lut,
   });
 }
 
+int gpcx_lut_correct_from_hist_device(const uint32_t* hist, int mode, const uint16_t* in,
+                                      uint16_t* out, uint64_t n, uint16_t* lut,
+                                      gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
+                                      void* stream) {
+  return guarded([&] {
+    if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    gpcx::lut::launch_correct_from_hist(hist, mode, in, out, n, lut, stats, ws,
+                                        as_stream(stream));
+  });
+}
+
 int gpcx_lut_minmax_device(const uint16_t* img, uint64_t n, gpcx_lut_stats* stats, void* ws,
                            uint64_t ws_bytes, void* stream) {
   return guarded([&] {

@@ -179,7 +179,12 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       } else if (equalize) {
         GPCX_CUDA(cudaMemcpyAsync(s.d_hist(), global_hist.data(), 65536 * 4,
                                   cudaMemcpyHostToDevice, s.stream));
-        lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr, s.stream);
+        if (need_apply)  // LUT from the merged histogram + apply: one launch
+          lut::launch_correct_from_hist(s.d_hist(), p.mode, dimg, dimg, bn, s.d_lut(),
+                                        s.d_stats(), s.lut_ws.ptr, s.stream);
+        else
+          lut::launch_from_hist(s.d_hist(), p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr,
+                                s.stream);
       } else {
         GPCX_CUDA(cudaMemcpyAsync(s.d_stats(), &global_mm, sizeof(global_mm),
                                   cudaMemcpyHostToDevice, s.stream));
@@ -189,7 +194,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
                                 cudaMemcpyDeviceToHost, s.stream));
     }
     if (need_apply) {
-      if (!(G == 1 && equalize && flag != Flag::LutApply))  // else applied by the fused launch
+      if (!(equalize && flag != Flag::LutApply))  // else applied by the fused launch
         lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
       rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
       if (lut_out != nullptr && i == 0)

@@ -30,12 +30,18 @@ std::uint32_t* ws_hist(void* ws);
 
 int parts_for(std::uint64_t n, int num_sms);
 
+// Histogram of img into hist (u32[65536]).
 void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
                  void* ws, cudaStream_t stream);
-// LUT + stats from a merged histogram (cooperative build kernel; `ws` is a
-// LUT workspace, used for the per-CTA scan triples).
+// LUT + stats from a merged histogram (`ws` is a LUT workspace, used for the
+// per-slice scan summaries).
 void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,
                       gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+// LUT from a merged (e.g. all-reduced) histogram, then out = LUT[in]: one
+// launch when in/out are co-aligned.  The second half of a sharded LUT_CORRECT.
+void launch_correct_from_hist(const std::uint32_t* hist, int mode, const std::uint16_t* in,
+                              std::uint16_t* out, std::uint64_t n, std::uint16_t* lut,
+                              gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 // Single-device LUT_GEN equalize: one cooperative fused_kernel launch
 // (the histogram lands in ws_hist(ws)).
 void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,

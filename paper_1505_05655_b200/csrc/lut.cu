@@ -7,17 +7,14 @@
 // GPU count (the parexec invariance contract, proj/include/gpc/parexec.hpp:11-31).
 //
 // Kernels (see DESIGN.md for the roofline of each):
-//   fused_kernel    single-device equalize LUT_GEN / LUT_CORRECT in one
-//                   cooperative launch: histogram -> merge -> LUT [-> apply].
-//   hist_kernel     persistent, 1 CTA/SM, 128 KiB smem histogram of packed
-//                   u16 pairs, 128-bit streaming loads.   2 B/px read.
-//                   (multi-GPU: local histogram before the all-reduce)
-//   merge_kernel    column-sum of the per-CTA partials (+ overflow fixups).
-//   build_kernel    cooperative LUT build from a (all-reduced) histogram.
+//   fused_kernel    the equalize path, one cooperative launch, phases
+//                   selected per call: histogram (1 CTA/SM, 128 KiB smem of
+//                   packed u16 pairs, 128-bit streaming loads, 2 B/px) ->
+//                   partial merge -> LUT -> apply (4 B/px).
 //   minmax_kernel   warp-shuffle (redux) min/max for stretch.  2 B/px read.
 //   from_minmax     stretch LUT.
-//   apply_kernel    persistent, LUT staged in 128 KiB smem, 128-bit
-//                   loads/stores, 8 gathers per vector.   4 B/px.
+//   apply_kernel    LUT_APPLY: persistent, LUT staged in 128 KiB smem,
+//                   128-bit loads/stores, 8 gathers per vector.   4 B/px.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -209,53 +206,6 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
   for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    hist_kernel(const std::uint16_t* __restrict__ img, std::uint64_t n,
-                uint32_t* __restrict__ parts,
-                uint32_t* __restrict__ overflow) {
-  extern __shared__ uint4 smem_u4[];
-  uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
-  for (int i = threadIdx.x; i < kWords / 4; i += kThreads)
-    smem_u4[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-
-  count_image(img, n, blockIdx.x, gridDim.x, bins, overflow);
-  __syncthreads();
-
-  uint4* dst = reinterpret_cast<uint4*>(parts + static_cast<std::uint64_t>(blockIdx.x) * kWords);
-  for (int j = threadIdx.x; j < kWords / 4; j += kThreads) dst[j] = smem_u4[j];
-}
-
-// hist[2w], hist[2w+1] = column sums of the packed partials + overflow;
-// leaves the overflow counters zeroed for the next call.
-__global__ void __launch_bounds__(256)
-    merge_kernel(const uint32_t* __restrict__ parts, int nparts,
-                 uint32_t* __restrict__ overflow,
-                 uint32_t* __restrict__ hist) {
-  const int w = blockIdx.x * 256 + threadIdx.x;
-  if (w >= kWords) return;
-  uint32_t lo = 0, hi = 0;
-  int p = 0;
-  for (; p + 4 <= nparts; p += 4) {
-    uint32_t x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = parts[static_cast<std::uint64_t>(p + u) * kWords + w];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      lo += x[u] & 0xFFFFu;
-      hi += x[u] >> 16;
-    }
-  }
-  for (; p < nparts; ++p) {
-    const uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
-    lo += x & 0xFFFFu;
-    hi += x >> 16;
-  }
-  const uint2 ov = reinterpret_cast<const uint2*>(overflow)[w];
-  reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
-  reinterpret_cast<uint2*>(hist)[w] = make_uint2(lo + ov.x, hi + ov.y);
-}
-
 // floor(num / d) for num < 2^50 and d >= 1 without a 64-bit integer divide
 // (a ~70-instruction software sequence): the f64 estimate num * (1/d) is
 // within 1/8 of the true quotient, so truncation is off by at most one and a
@@ -292,120 +242,6 @@ __device__ __forceinline__ uint32_t stretch_entry(std::uint64_t v,
       udiv_exact((v - lo) * 65535u + span / 2, span, 1.0 / static_cast<double>(span)));
 }
 
-// Fused histogram merge + LUT build, one cooperative grid of 128 CTAs x 256
-// threads (every CTA resident): thread t of CTA b owns bins 2w, 2w+1 with
-// w = 256b + t.
-//   phase 1  merge the per-CTA packed partials (+ overflow, which it zeroes)
-//            into hist[] -- or take hist[] as given (multi-GPU: all-reduced)
-//            -- and publish per-CTA totals / first / last non-empty bins;
-//   grid.sync
-//   phase 2  every CTA derives n, lo, hi and its cdf offset from the 128
-//            published triples, scans its 512 bins and writes its LUT slice.
-constexpr int kBuildCtas = kWords / 256;  // 128
-
-__global__ void __launch_bounds__(256)
-    build_kernel(const uint32_t* __restrict__ parts, int nparts,
-                 uint32_t* __restrict__ overflow, uint32_t* __restrict__ hist,
-                 int merge, int mode, uint3* __restrict__ blocks,
-                 std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats) {
-  __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int w = blockIdx.x * 256 + t;
-  uint32_t c0, c1;
-  if (merge) {
-    uint32_t lo = 0, hi = 0;
-    int p = 0;
-    for (; p + 4 <= nparts; p += 4) {
-      uint32_t x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = parts[static_cast<std::uint64_t>(p + u) * kWords + w];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        lo += x[u] & 0xFFFFu;
-        hi += x[u] >> 16;
-      }
-    }
-    for (; p < nparts; ++p) {
-      const uint32_t x = parts[static_cast<std::uint64_t>(p) * kWords + w];
-      lo += x & 0xFFFFu;
-      hi += x >> 16;
-    }
-    const uint2 ov = reinterpret_cast<const uint2*>(overflow)[w];
-    reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
-    c0 = lo + ov.x;
-    c1 = hi + ov.y;
-    reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
-  } else {
-    const uint2 h = reinterpret_cast<const uint2*>(hist)[w];
-    c0 = h.x;
-    c1 = h.y;
-  }
-  // CTA totals: warp inclusive scan of (c0 + c1), then across 8 warps.
-  const uint32_t pair = c0 + c1;
-  uint32_t inc = pair;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += y;
-  }
-  const uint32_t first = c0 ? 2u * w : (c1 ? 2u * w + 1 : 0xFFFFFFFFu);
-  const uint32_t last = c1 ? 2u * w + 1 : (c0 ? 2u * w : 0u);
-  const uint32_t wfirst = __reduce_min_sync(0xFFFFFFFFu, first);
-  const uint32_t wlast = __reduce_max_sync(0xFFFFFFFFu, last);
-  if (lane == 31) s_wsum[warp] = inc;
-  if (lane == 0) {
-    s_wfirst[warp] = wfirst;
-    s_wlast[warp] = wlast;
-  }
-  __syncthreads();
-  uint32_t warp_off = 0, cta_sum = 0, cta_first = 0xFFFFFFFFu, cta_last = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < warp) warp_off += s_wsum[i];
-    cta_sum += s_wsum[i];
-    cta_first = min(cta_first, s_wfirst[i]);
-    cta_last = max(cta_last, s_wlast[i]);
-  }
-  if (t == 0) blocks[blockIdx.x] = make_uint3(cta_sum, cta_first, cta_last);
-  cg::this_grid().sync();
-
-  // Phase 2: global n / lo / hi and this CTA's offset from the 128 triples.
-  uint32_t n32 = 0, off = 0, lo = 0xFFFFFFFFu, hi = 0;
-  for (int b = lane; b < kBuildCtas; b += 32) {
-    const uint3 q = blocks[b];
-    n32 += q.x;
-    if (b < static_cast<int>(blockIdx.x)) off += q.x;
-    lo = min(lo, q.y);
-    if (q.x != 0) hi = max(hi, q.z);
-  }
-  n32 = __reduce_add_sync(0xFFFFFFFFu, n32);
-  off = __reduce_add_sync(0xFFFFFFFFu, off);
-  lo = __reduce_min_sync(0xFFFFFFFFu, lo);
-  hi = __reduce_max_sync(0xFFFFFFFFu, hi);
-  const uint32_t v0 = 2u * w;
-  uint32_t e0, e1;
-  if (lo == 0xFFFFFFFFu) {  // empty image: identity LUT, zero stats
-    e0 = v0;
-    e1 = v0 + 1;
-    if (w == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
-  } else {
-    const std::uint64_t n = n32;
-    const std::uint64_t cdf_min = hist[lo];
-    if (w == 0) *stats = gpcx_lut_stats{n, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
-    if (mode == GPCX_LUT_STRETCH) {
-      e0 = stretch_entry(v0, n, lo, hi);
-      e1 = stretch_entry(v0 + 1, n, lo, hi);
-    } else {
-      const std::uint64_t d = n - cdf_min;
-      const double inv_d = d != 0 ? 1.0 / static_cast<double>(d) : 0.0;
-      const std::uint64_t cdf1 = static_cast<std::uint64_t>(off) + warp_off + inc;  // through v0+1
-      e0 = equalize_entry(v0, cdf1 - c1, cdf_min, d, inv_d, lo);
-      e1 = equalize_entry(v0 + 1, cdf1, cdf_min, d, inv_d, lo);
-    }
-  }
-  reinterpret_cast<uint32_t*>(lut)[w] = e0 | (e1 << 16);
-}
-
 #ifdef GPCX_LUT_TRACE
 // Phase timestamps for tools/fused_trace.cu (compiled out of the library).
 __device__ unsigned long long* g_lut_trace;
@@ -421,22 +257,28 @@ __device__ unsigned long long* g_lut_trace;
 #define LUT_STAMP(k) do {} while (0)
 #endif
 
-// The whole single-device equalize LUT_GEN / LUT_CORRECT in ONE cooperative
-// launch, 1 CTA x 1024 threads per SM (every CTA resident):
-//   phase 1  CTAs < nparts count their share of the image into packed smem
-//            bins and flush them as partials;                      grid.sync
-//   phase 2  CTA b < 128 owns bins [512b, 512b + 512): 16 groups of 64
-//            threads column-sum 1/16 of the partials each with 128-bit
-//            loads (16x the memory-level parallelism of one thread per
-//            word), a smem reduction joins the groups, + overflow (zeroed
-//            for the next call); publishes the CTA's total / first / last
-//            non-empty bin;                                        grid.sync
-//   phase 3  each of those CTAs derives n, lo, hi and its cdf offset from the
-//            128 triples and writes its 512 LUT entries;  [apply:] grid.sync
-//   phase 4  every CTA stages the LUT in smem (over the dead bins) and maps
-//            the image -- which, at C1 size, phase 1 left in L2.
-// Replaces hist_kernel + build_kernel (+ apply_kernel): no launch gaps, and
-// the partial merge is no longer latency-bound (~17 us -> a few us).
+// The equalize LUT path as ONE cooperative kernel, 1 CTA x 1024 threads per
+// SM (every CTA resident); `stages` selects the phases:
+//   kCount   phase 1  CTAs < nparts count their share of the image into packed
+//                     smem bins and flush them as partials;        grid.sync
+//            phase 2  CTA b < 128 owns bins [512b, 512b + 512): 16 groups of
+//                     64 threads column-sum 1/16 of the partials each with
+//                     128-bit loads (16x the memory-level parallelism of one
+//                     thread per word), a smem reduction joins the groups,
+//                     + overflow (zeroed for the next call) -> hist[];
+//            without kCount phase 2 takes hist[] as given (multi-GPU: the
+//            all-reduced histogram).  Each slice publishes (total, first,
+//            last non-empty bin, count of first).
+//   kBuild   grid.sync; phase 3  each slice CTA derives n, lo, hi, cdf_min and
+//                     its cdf offset from the 128 summaries and writes its
+//                     512 LUT entries;
+//   kApply   grid.sync; phase 4  every CTA stages the LUT in smem (over the dead
+//                     bins) and maps the image -- which, at C1 size, phase 1
+//                     left in L2.
+// Single device LUT_CORRECT = kCount|kBuild|kApply, LUT_GEN = kCount|kBuild;
+// N devices: kCount -> all-reduce(hist) -> kBuild|kApply.  No launch gaps,
+// and the partial merge is not latency-bound like a one-thread-per-bin sum.
+enum Stage : int { kCount = 1, kBuild = 2, kApply = 4 };
 constexpr int kSlices = kWords / 256;    // 128 CTAs own 512 bins in phases 2-3
 constexpr int kGroups = kThreads / 64;   // partial groups per slice
 static_assert(kGroups * 512 * 4 <= kWords * 4, "phase-2 reduction fits in the bins");
@@ -446,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  uint32_t* __restrict__ parts, uint32_t* __restrict__ overflow,
                  uint32_t* __restrict__ hist, uint4* __restrict__ blocks, int mode,
                  std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
-                 int apply) {
+                 int stages) {
   extern __shared__ uint4 smem_u4[];
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
   __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8], s_wfcount[8];
@@ -454,8 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
   LUT_STAMP(0);
+  const bool count = stages & kCount;
   // ---- phase 1: per-CTA histograms
-  if (static_cast<int>(blockIdx.x) < nparts) {
+  if (count && static_cast<int>(blockIdx.x) < nparts) {
     for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     count_image(img, n, blockIdx.x, nparts, bins, overflow);
@@ -465,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = t; j < kWords / 4; j += kThreads) dst[j] = smem_u4[j];
   }
   LUT_STAMP(2);
-  grid.sync();
+  if (count) grid.sync();
   LUT_STAMP(3);
 
   // ---- phase 2: merge this CTA's 512-bin slice
@@ -473,41 +316,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int w = blockIdx.x * 256 + t;  // word (bins 2w, 2w+1) of threads t < 256
   uint32_t c0 = 0, c1 = 0, inc = 0;
   if (slice_cta) {
-    const int quad = t & 63, group = t >> 6;
-    const uint4* pq = reinterpret_cast<const uint4*>(parts) + blockIdx.x * 64 + quad;
-    constexpr std::uint64_t kPartQuads = kWords / 4;
-    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    auto add = [&](uint4 x) {
-      acc[0] += x.x & 0xFFFFu; acc[1] += x.x >> 16;
-      acc[2] += x.y & 0xFFFFu; acc[3] += x.y >> 16;
-      acc[4] += x.z & 0xFFFFu; acc[5] += x.z >> 16;
-      acc[6] += x.w & 0xFFFFu; acc[7] += x.w >> 16;
-    };
-    int p = group;
-    for (; p + 7 * kGroups < nparts; p += 8 * kGroups) {  // 8 loads in flight
-      uint4 x[8];
+    if (count) {
+      const int quad = t & 63, group = t >> 6;
+      const uint4* pq = reinterpret_cast<const uint4*>(parts) + blockIdx.x * 64 + quad;
+      constexpr std::uint64_t kPartQuads = kWords / 4;
+      uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      auto add = [&](uint4 x) {
+        acc[0] += x.x & 0xFFFFu; acc[1] += x.x >> 16;
+        acc[2] += x.y & 0xFFFFu; acc[3] += x.y >> 16;
+        acc[4] += x.z & 0xFFFFu; acc[5] += x.z >> 16;
+        acc[6] += x.w & 0xFFFFu; acc[7] += x.w >> 16;
+      };
+      int p = group;
+      for (; p + 7 * kGroups < nparts; p += 8 * kGroups) {  // 8 loads in flight
+        uint4 x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldcg(pq + (p + u * kGroups) * kPartQuads);
+        for (int u = 0; u < 8; ++u) x[u] = __ldcg(pq + (p + u * kGroups) * kPartQuads);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) add(x[u]);
+        for (int u = 0; u < 8; ++u) add(x[u]);
+      }
+      for (; p < nparts; p += kGroups) add(__ldcg(pq + p * kPartQuads));
+      // red[group][bin], bin = 8 * quad + j of the slice
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
     }
-    for (; p < nparts; p += kGroups) add(__ldcg(pq + p * kPartQuads));
-    // red[group][bin], bin = 8 * quad + j of the slice
-#pragma unroll
-    for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
     __syncthreads();
     if (t < 256) {
-      uint32_t lo = 0, hi = 0;
+      if (count) {
+        uint32_t lo = 0, hi = 0;
 #pragma unroll
-      for (int g = 0; g < kGroups; ++g) {
-        lo += bins[g * 512 + 2 * t];
-        hi += bins[g * 512 + 2 * t + 1];
+        for (int g = 0; g < kGroups; ++g) {
+          lo += bins[g * 512 + 2 * t];
+          hi += bins[g * 512 + 2 * t + 1];
+        }
+        const uint2 ov = __ldcg(reinterpret_cast<const uint2*>(overflow) + w);
+        reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
+        c0 = lo + ov.x;
+        c1 = hi + ov.y;
+        reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
+      } else {
+        const uint2 h = __ldcg(reinterpret_cast<const uint2*>(hist) + w);
+        c0 = h.x;
+        c1 = h.y;
       }
-      const uint2 ov = __ldcg(reinterpret_cast<const uint2*>(overflow) + w);
-      reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
-      c0 = lo + ov.x;
-      c1 = hi + ov.y;
-      reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
       inc = c0 + c1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -545,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   LUT_STAMP(4);
+  if (!(stages & kBuild)) return;
   grid.sync();
   LUT_STAMP(5);
 
@@ -598,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     reinterpret_cast<uint32_t*>(lut)[w] = e0 | (e1 << 16);
   }
   LUT_STAMP(6);
-  if (!apply) return;
+  if (!(stages & kApply)) return;
   grid.sync();
   LUT_STAMP(7);
 
@@ -750,7 +602,7 @@ void set_attrs_once() {
   int dev = 0;
   GPCX_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && g_attrs_set[dev]) return;
-  GPCX_CUDA(cudaFuncSetAttribute(hist_kernel,
+  GPCX_CUDA(cudaFuncSetAttribute(fused_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemHist));
   GPCX_CUDA(cudaFuncSetAttribute(apply_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLut));
@@ -775,80 +627,67 @@ int parts_for(std::uint64_t n, int num_sms) {
   return std::max(1, std::min(p, kMaxParts));
 }
 
-void launch_hist(const std::uint16_t* img, std::uint64_t n, uint32_t* hist,
-                 void* ws, cudaStream_t stream) {
+namespace {
+// fused_kernel over the whole device (see its comment for `stages`).
+void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std::uint64_t n,
+                  uint32_t* hist, int mode, std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
+                  cudaStream_t stream) {
   set_attrs_once();
   auto* base = static_cast<unsigned char*>(ws);
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
   auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
-  const int p = parts_for(n, device_sm_count());
-  hist_kernel<<<p, kThreads, kSmemHist, stream>>>(img, n, parts, overflow);
-  GPCX_LAUNCH_CHECK();
-  merge_kernel<<<kWords / 256, 256, 0, stream>>>(parts, p, overflow, hist);
-  GPCX_LAUNCH_CHECK();
-}
-
-namespace {
-void launch_build(const uint32_t* parts, int nparts, uint32_t* overflow,
-                  uint32_t* hist, int merge, int mode, void* ws, std::uint16_t* lut,
-                  gpcx_lut_stats* stats, cudaStream_t stream) {
-  auto* blocks = reinterpret_cast<uint3*>(static_cast<unsigned char*>(ws) + kBlocksOff);
-  void* args[] = {&parts, &nparts, &overflow, &hist, &merge, &mode, &blocks, &lut, &stats};
-  GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(build_kernel),
-                                        dim3(kBuildCtas), dim3(256), args, 0, stream));
-}
-}  // namespace
-
-void launch_from_hist(const uint32_t* hist, int mode, std::uint16_t* lut,
-                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
-  launch_build(nullptr, 0, nullptr, const_cast<uint32_t*>(hist), 0, mode, ws, lut, stats,
-               stream);
-}
-
-namespace {
-// fused_kernel over the whole device; `out` == nullptr -> LUT_GEN only.
-void launch_fused(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int mode,
-                  std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
-  static bool attr_set[64] = {};
-  int dev = 0;
-  GPCX_CUDA(cudaGetDevice(&dev));
-  if (dev >= 64 || !attr_set[dev]) {
-    GPCX_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kSmemHist));
-    if (dev < 64) attr_set[dev] = true;
-  }
-  auto* base = static_cast<unsigned char*>(ws);
-  auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
-  auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
-  auto* hist = reinterpret_cast<uint32_t*>(base + kHistOff);
   auto* blocks = reinterpret_cast<uint4*>(base + kBlocksOff);
+  if (hist == nullptr) hist = reinterpret_cast<uint32_t*>(base + kHistOff);
   const int sms = device_sm_count();
   int nparts = parts_for(n, sms);
-  int apply = out != nullptr;
-  std::uint16_t* dst = out;
-  void* args[] = {const_cast<std::uint16_t**>(&img), &dst, &n, &nparts, &parts, &overflow,
-                  &hist, &blocks, &mode, &lut, &stats, &apply};
+  void* args[] = {const_cast<std::uint16_t**>(&img), &out, &n, &nparts, &parts, &overflow,
+                  &hist, &blocks, &mode, &lut, &stats, &stages};
   GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fused_kernel),
                                         dim3(std::max(sms, kSlices)), dim3(kThreads), args,
                                         kSmemHist, stream));
 }
+
+bool co_aligned(const void* a, const void* b) {
+  return ((reinterpret_cast<std::uintptr_t>(a) ^ reinterpret_cast<std::uintptr_t>(b)) & 15u) == 0;
+}
 }  // namespace
+
+void launch_hist(const std::uint16_t* img, std::uint64_t n, uint32_t* hist,
+                 void* ws, cudaStream_t stream) {
+  launch_fused(kCount, img, nullptr, n, hist, GPCX_LUT_EQUALIZE, nullptr, nullptr, ws, stream);
+}
+
+void launch_from_hist(const uint32_t* hist, int mode, std::uint16_t* lut,
+                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  launch_fused(kBuild, nullptr, nullptr, 0, const_cast<uint32_t*>(hist), mode, lut, stats, ws,
+               stream);
+}
+
+void launch_correct_from_hist(const uint32_t* hist, int mode, const std::uint16_t* in,
+                              std::uint16_t* out, std::uint64_t n, std::uint16_t* lut,
+                              gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+  if (co_aligned(in, out) && n != 0) {
+    launch_fused(kBuild | kApply, in, out, n, const_cast<uint32_t*>(hist), mode, lut, stats, ws,
+                 stream);
+    return;
+  }
+  launch_from_hist(hist, mode, lut, stats, ws, stream);
+  launch_apply(lut, in, out, n, stream);
+}
 
 void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::uint16_t* lut,
                      gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
-  launch_fused(img, nullptr, n, mode, lut, stats, ws, stream);
+  launch_fused(kCount | kBuild, img, nullptr, n, nullptr, mode, lut, stats, ws, stream);
 }
 
 void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
                     std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
-  const bool vector_ok =
-      ((reinterpret_cast<std::uintptr_t>(in) ^ reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
-  if (mode == GPCX_LUT_EQUALIZE && vector_ok && n != 0) {
-    launch_fused(in, out, n, mode, lut, stats, ws, stream);
+  if (mode == GPCX_LUT_EQUALIZE && co_aligned(in, out) && n != 0) {
+    launch_fused(kCount | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream);
     return;
   }
   if (mode == GPCX_LUT_EQUALIZE) {
-    launch_fused(in, nullptr, n, mode, lut, stats, ws, stream);
+    launch_hist_lut(in, n, mode, lut, stats, ws, stream);
   } else {
     launch_minmax(in, n, stats, ws, stream);
     launch_from_minmax(stats, lut, stream);

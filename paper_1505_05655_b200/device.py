@@ -54,6 +54,12 @@ def lut_from_hist(hist, mode, lut, stats, ws, stream=None):
                                         _s(stream)))
 
 
+def lut_correct_from_hist(hist, mode, inp, out, lut, stats, ws, stream=None):
+    check(lib.gpcx_lut_correct_from_hist_device(_p(hist), mode, _p(inp), _p(out), inp.numel(),
+                                                _p(lut), _p(stats), _p(ws), ws.numel(),
+                                                _s(stream)))
+
+
 def lut_minmax(img, stats, ws, stream=None):
     check(lib.gpcx_lut_minmax_device(_p(img), img.numel(), _p(stats), _p(ws), ws.numel(), _s(stream)))
 

@@ -139,6 +139,33 @@ def test_lut_correct_fused_alignment_and_inplace(gpu, in_off, out_off):
     assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
 
 
+@pytest.mark.parametrize("mode,mname", MODES)
+def test_sharded_correct_from_summed_band_histograms(gpu, mode, mname):
+    """The N-GPU step on one device: per-band histograms (count stage),
+    summed like the all-reduce, then LUT + apply per band
+    (gpcx_lut_correct_from_hist_device) == the whole-image oracle."""
+    torch, D = _dev()
+    rows, cols = 1001, 777
+    img = D.synth_image(O.IMG_RAMP12, 12, rows, cols)
+    ref_out, ref_lut, ref_st = O.lut_correct(u16(img), mode)
+    per = (rows + 2) // 3
+    bands = [img[r * cols:min(rows, r + per) * cols] for r in range(0, rows, per)]
+    total = torch.zeros(65536, dtype=torch.int64, device=gpu)
+    ws = D.lut_workspace(img.numel())
+    for b in bands:
+        h = torch.zeros(65536, dtype=torch.int32, device=gpu)
+        D.lut_hist(b, h, ws)
+        total += h.to(torch.int64)
+    hist = total.to(torch.int32)
+    out = torch.empty_like(img)
+    outs = [out[r * cols:min(rows, r + per) * cols] for r in range(0, rows, per)]
+    for b, o in zip(bands, outs):
+        lut, stats = D.new_lut(), D.new_stats()
+        D.lut_correct_from_hist(hist, mode, b, o, lut, stats, ws)
+        assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
+    assert np.array_equal(u16(out), ref_out)
+
+
 def test_lut_correct_fused_counter_wraps_and_reuse(gpu):
     """Packed-counter wraps through the fused path, twice on one workspace
     (the overflow counters must come back zeroed)."""
