@@ -1,7 +1,5 @@
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_all.log 2>&1; tail -3 gpurun_out/t_all.log
-GPCX_BENCH_ONE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 --workload lut > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; tail -c 300 gpurun_out/bench_n2.err
-python -c "
-import json;d=json.loads(open('gpurun_out/bench_n2.json').read().strip().splitlines()[-1]);print(json.dumps({k:d.get(k) for k in ('value','ms_per_step','roofline','gpu_launches')})[:1200])"
-timeout 900 python bench.py --workload lut --steps 20 --warmup 5 > gpurun_out/bench_lut.json 2> gpurun_out/bench_lut.err; tail -c 300 gpurun_out/bench_lut.err
-python -c "
-import json;d=json.loads(open('gpurun_out/bench_lut.json').read().strip().splitlines()[-1]);print(json.dumps({k:d.get(k) for k in ('value','ms_per_step','roofline','gpu_launches')})[:1200])"
+timeout 900 python -m pytest tests/test_matmul_gpu.py -x -q -m gpu > gpurun_out/t_mm.log 2>&1; tail -3 gpurun_out/t_mm.log
+for rep in 1 2; do
+  C4N=16384 timeout 300 python tools/c4_ab.py 2sm 2sm512 2>/dev/null | sed "s/^/16k /"
+  timeout 300 python tools/c4_ab.py 2sm 2sm512 2>/dev/null | sed "s/^/32k /"
+done
