@@ -589,42 +589,105 @@ __device__ __forceinline__ float round_tf32(float x) {
   return __uint_as_float(r);
 }
 
-// A (m x k, lda) -> A' (m x kp), K-major; zero padding beyond k.
+// 8 operand values -> their prepared form (bf16 RNE: one uint4; tf32 RNA:
+// two float4), stored at dst (16-byte aligned).
 template <bool kTf32>
-__global__ void prep_a_kernel(const float* __restrict__ A, std::uint64_t lda, int m, int k, int kp,
-                              void* __restrict__ out) {
-  const std::uint64_t total = static_cast<std::uint64_t>(m) * kp;
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += stride) {
-    const std::uint64_t r = i / kp, c = i % kp;
-    const float x = c < static_cast<std::uint64_t>(k) ? A[r * lda + c] : 0.f;
-    if constexpr (kTf32) static_cast<float*>(out)[i] = round_tf32(x);
-    else static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(x);
+__device__ __forceinline__ void store8(void* dst, const float (&x)[8]) {
+  if constexpr (kTf32) {
+    float4* d = static_cast<float4*>(dst);
+    d[0] = make_float4(round_tf32(x[0]), round_tf32(x[1]), round_tf32(x[2]), round_tf32(x[3]));
+    d[1] = make_float4(round_tf32(x[4]), round_tf32(x[5]), round_tf32(x[6]), round_tf32(x[7]));
+  } else {
+    uint4 v;
+    std::uint32_t* w = reinterpret_cast<std::uint32_t*>(&v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+      w[j] = *reinterpret_cast<const std::uint32_t*>(&h);
+    }
+    *static_cast<uint4*>(dst) = v;
   }
 }
 
-// B (k x n, ldb) -> B'^T (n x kp), K-major, through a 32 x 33 smem tile.
+// A (m x k, lda) -> A' (m x kp), K-major; zero padding beyond k.  One warp
+// per row at a time, 8 consecutive values per lane per step (two 128-bit
+// loads when A is 16-byte aligned with lda % 4 == 0; one 16- or 32-byte
+// store).  HBM-bound: 4 B read + 2 (bf16) / 4 (tf32) B written per value.
 template <bool kTf32>
-__global__ void prep_bt_kernel(const float* __restrict__ B, std::uint64_t ldb, int k, int n, int kp,
-                               void* __restrict__ out) {
-  __shared__ float tile[32][33];
-  const int k0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+__global__ void __launch_bounds__(256)
+    prep_a_kernel(const float* __restrict__ A, std::uint64_t lda, int m, int k, int kp,
+                  void* __restrict__ out) {
+  constexpr int kEs = kTf32 ? 4 : 2;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * 8;
+  const bool vec = ((reinterpret_cast<std::uintptr_t>(A) & 15) == 0) && (lda % 4 == 0);
+  const int chunks = kp / 8;
+  for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < m; r += warps) {
+    const float* src = A + static_cast<std::uint64_t>(r) * lda;
+    auto* dst = static_cast<std::uint8_t*>(out) + static_cast<std::uint64_t>(r) * kp * kEs;
+    for (int c = lane; c < chunks; c += 32) {
+      const int c0 = c * 8;
+      float x[8];
+      if (vec && c0 + 8 <= k) {
+        const float4 p = __ldcs(reinterpret_cast<const float4*>(src + c0));
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(src + c0 + 4));
+        x[0] = p.x; x[1] = p.y; x[2] = p.z; x[3] = p.w;
+        x[4] = q.x; x[5] = q.y; x[6] = q.z; x[7] = q.w;
+      } else {
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    const int kk = k0 + ty + j, nn = n0 + tx;
-    tile[ty + j][tx] = (kk < k && nn < n) ? B[static_cast<std::uint64_t>(kk) * ldb + nn] : 0.f;
+        for (int j = 0; j < 8; ++j) x[j] = c0 + j < k ? src[c0 + j] : 0.f;
+      }
+      store8<kTf32>(dst + static_cast<std::uint64_t>(c0) * kEs, x);
+    }
+  }
+}
+
+// B (k x n, ldb) -> B'^T (n x kp), K-major.  64 (k) x 64 (n) tile per CTA
+// through smem (row pitch 65 floats: conflict-free column reads); loads
+// are 128-bit along n, stores 8 consecutive k values (16 / 32 B) per lane,
+// 8 lanes per output row = 128 / 256 contiguous bytes.
+template <bool kTf32>
+__global__ void __launch_bounds__(256)
+    prep_bt_kernel(const float* __restrict__ B, std::uint64_t ldb, int k, int n, int kp,
+                   void* __restrict__ out) {
+  constexpr int kEs = kTf32 ? 4 : 2;
+  __shared__ float tile[64][65];
+  const int k0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int t = threadIdx.x;
+  const bool vec = ((reinterpret_cast<std::uintptr_t>(B) & 15) == 0) && (ldb % 4 == 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = t + 256 * i;           // 1024 float4 slots
+    const int kk = idx >> 4, nn = (idx & 15) * 4;
+    const int gk = k0 + kk, gn = n0 + nn;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (gk < k) {
+      const float* row = B + static_cast<std::uint64_t>(gk) * ldb;
+      if (vec && gn + 4 <= n) {
+        const float4 p = __ldcs(reinterpret_cast<const float4*>(row + gn));
+        v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (gn + j < n) v[j] = row[gn + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tile[kk][nn + j] = v[j];
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    const int nn = n0 + ty + j, kk = k0 + tx;
-    if (nn < n && kk < kp) {
-      const float x = tile[tx][ty + j];
-      const std::uint64_t o = static_cast<std::uint64_t>(nn) * kp + kk;
-      if constexpr (kTf32) static_cast<float*>(out)[o] = round_tf32(x);
-      else static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(x);
+  for (int i = 0; i < 2; ++i) {
+    const int idx = t + 256 * i;           // 512 (row, 8-value chunk) slots
+    const int nn = idx >> 3, kc = (idx & 7) * 8;
+    const int gn = n0 + nn, gk = k0 + kc;
+    if (gn < n && gk < kp) {
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = tile[kc + j][nn];
+      store8<kTf32>(static_cast<std::uint8_t*>(out) +
+                        (static_cast<std::uint64_t>(gn) * kp + gk) * kEs,
+                    x);
     }
   }
 }
@@ -716,15 +779,14 @@ void launch_tc(int prec, std::uint64_t m, std::uint64_t n, std::uint64_t k, cons
 
   const int sms = device_sm_count();
   {
-    const std::uint64_t total = m * kp;
-    const int grid = static_cast<int>(std::min<std::uint64_t>((total + 255) / 256, 16ull * sms));
-    if (tf32) prep_a_kernel<true><<<grid, 256, 0, stream>>>(A, lda, (int)m, (int)k, (int)kp, a_p);
-    else prep_a_kernel<false><<<grid, 256, 0, stream>>>(A, lda, (int)m, (int)k, (int)kp, a_p);
+    const int grid_a = static_cast<int>(std::min<std::uint64_t>((m + 7) / 8, 32ull * sms));
+    if (tf32) prep_a_kernel<true><<<grid_a, 256, 0, stream>>>(A, lda, (int)m, (int)k, (int)kp, a_p);
+    else prep_a_kernel<false><<<grid_a, 256, 0, stream>>>(A, lda, (int)m, (int)k, (int)kp, a_p);
     GPCX_LAUNCH_CHECK();
-    const dim3 g2(static_cast<unsigned>((kp + 31) / 32), static_cast<unsigned>((n + 31) / 32));
+    const dim3 g2(static_cast<unsigned>((kp + 63) / 64), static_cast<unsigned>((n + 63) / 64));
     if (g2.y > 65535) fail(Errc::TooLarge, "n too large for the transpose grid");
-    if (tf32) prep_bt_kernel<true><<<g2, dim3(32, 8), 0, stream>>>(B, ldb, (int)k, (int)n, (int)kp, b_p);
-    else prep_bt_kernel<false><<<g2, dim3(32, 8), 0, stream>>>(B, ldb, (int)k, (int)n, (int)kp, b_p);
+    if (tf32) prep_bt_kernel<true><<<g2, 256, 0, stream>>>(B, ldb, (int)k, (int)n, (int)kp, b_p);
+    else prep_bt_kernel<false><<<g2, 256, 0, stream>>>(B, ldb, (int)k, (int)n, (int)kp, b_p);
     GPCX_LAUNCH_CHECK();
   }
 

@@ -189,3 +189,22 @@ def test_gpcx_run_matmul_block_rows_invariant(gpu, prec, m, k, n):
     rows = np.arange(0, m, 397)
     C = one.view(np.float32).reshape(m, n)
     _check(C, A, B, O.PREC_F32 if prec == "f32" else O.PREC_BF16, rows=rows)
+
+
+@pytest.mark.parametrize("prec", TC)
+@pytest.mark.parametrize("pad_a,pad_b", [(3, 1), (4, 4), (1, 7)])
+def test_tensor_core_operand_prep_strides(gpu, prec, pad_a, pad_b):
+    """Operand preparation on row pitches that break (or keep) 16-byte
+    alignment, and K / N not multiples of the 8-value chunks or 64-wide
+    transpose tiles: the prepared operands (and so C) stay exact."""
+    import torch
+    from paper_1505_05655_b200 import device as D
+    m, k, n = 333, 203, 141
+    A, B = _mats(O.MAT_UNIFORM32, 23, m, k, n)
+    big_a = torch.zeros(m, k + pad_a, device="cuda")
+    big_a[:, :k] = torch.from_numpy(A)
+    big_b = torch.zeros(k, n + pad_b, device="cuda")
+    big_b[:, :n] = torch.from_numpy(B)
+    Cm = torch.empty(m, n, device="cuda")
+    D.matmul(prec, big_a[:, :k], big_b[:, :n], Cm, D.matmul_workspace(prec, m, n, k))
+    _check(Cm.cpu().numpy(), A, B, prec)
