@@ -288,8 +288,10 @@ def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int =
             for _ in range(count):
                 one(p_in, p_out)
 
-        for _ in range(warmup):
-            one(*bufs[0])
+        for _ in range(warmup):  # at full concurrency: one request slot per in-flight request
+            ws = [th.Thread(target=worker, args=(k, *bufs[k], 1)) for k in range(inflight)]
+            [x.start() for x in ws]
+            [x.join() for x in ws]
         per = max(1, steps // inflight)
         t = time.perf_counter()
         ts = [th.Thread(target=worker, args=(k, *bufs[k], per)) for k in range(inflight)]
@@ -353,18 +355,19 @@ def matmul_device_leg(steps: int, warmup: int) -> dict:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     times = []
-    for i in range(warmup + steps):
-        flush.fill_(i & 0xFF)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        D.matmul(0, A, B, Cm, None, stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        if i >= warmup:
-            times.append(a.elapsed_time(b))
+    with Clocks(torch.cuda.current_device()) as clk:
+        for i in range(warmup + steps):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            D.matmul(0, A, B, Cm, None, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= warmup:
+                times.append(a.elapsed_time(b))
     ms = sum(times) / len(times)
     flops = 2.0 * MM ** 3
-    return {"ms": ms, "tflops": flops / ms / 1e9, "C": Cm}
+    return {"ms": ms, "tflops": flops / ms / 1e9, "C": Cm, "clocks": clk.summary()}
 
 
 def matmul_e2e_leg(steps: int) -> dict:
@@ -456,7 +459,11 @@ def c5_leg(n_gpus: int) -> dict:
     G.init(bound_devices(n_gpus))
     try:
         with G.Server(max_tasks=0) as srv:
-            c5_run(srv.port, imgs[:8], B, "bf16")  # warm-up: slots, pinned pools
+            # warm-up at the full concurrency: the first pass grows the
+            # server's request slots (device buffers) and pinned pools to 64
+            # requests in flight -- 3-6x slower than steady state
+            # (tools/c5_probe.py), and not what a running server pays
+            c5_run(srv.port, imgs, B, "bf16")
             res = c5_run(srv.port, imgs, B, "bf16")
     finally:
         G.init([0])
@@ -475,6 +482,7 @@ def cpu_c5() -> dict:
     from oracle import oracle as O
     imgs, B = c5_inputs()
     with O.RefServer(max_tasks=0) as rs:
+        c5_run(rs.port, imgs[:4], B, "bf16", 4)  # warm-up (no pools to grow: a short one)
         res = c5_run(rs.port, imgs[:C5_CPU_SAMPLE], B, "bf16", C5_CPU_SAMPLE)
     res.update({"kind": "port", "cores": O.max_threads(),
                 "sample": f"the first {C5_CPU_SAMPLE} chains of the same corpus, {C5_CPU_SAMPLE} concurrent "
@@ -532,10 +540,13 @@ def run_b200(args) -> None:
     mm = c4 = None
     if args.workload in ("all", "matmul"):
         torch.cuda.empty_cache()
-        c4 = matmul_c4_leg(d, max(2, min(args.steps, 5)), 1)
-        c4["ms_max"] = d.max(c4["ms"])
+        # C2 before C4: right after the 1 kW C4 GEMMs the power controller
+        # still holds the clock down for a while
         if d.rank == 0:
             mm = matmul_device_leg(max(3, min(args.steps, 10)), 2)
+        d.barrier()
+        c4 = matmul_c4_leg(d, max(2, min(args.steps, 5)), 1)
+        c4["ms_max"] = d.max(c4["ms"])
     d.barrier()
     if d.rank != 0:
         d.close()
@@ -575,6 +586,10 @@ def run_b200(args) -> None:
             # per step: fused_kernel once at N=1; count + build/apply launches at N>1
             "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": lut["clocks"]}
+    c5 = None
+    if args.workload in ("all", "c5"):
+        time.sleep(2)  # let the clock recover from the C4 leg
+        c5 = c5_leg(d.n)
     e2e_steps = max(4, min(args.steps, 8))
     e2e1 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=1)
     e2e2 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=2)
@@ -587,8 +602,6 @@ def run_b200(args) -> None:
                                       "ms_per_step": round(e2e1["ms_per_step"], 2)},
                    "path": "gpcx_lut_host (C ABI), pinned host buffers, all N GPUs in-process; "
                            "each step = one full C3 scene in (2 GiB H2D) and out (2 GiB D2H)"}
-    if d.n == 1:
-        line["cpu_baseline"] = cpu_lut(mode)
     if c4 is not None:
         flops = 2.0 * MM4 ** 3
         tf = flops / (c4["ms_max"] / 1e3) / 1e12
@@ -613,13 +626,16 @@ def run_b200(args) -> None:
                    "roofline": {"bound": "fp32-simt", "peak_note": "148 SMs x 128 FFMA x 2 x 1.965 GHz = 74.4 TFLOP/s nominal",
                                 "achieved": round(mm["tflops"], 2), "peak": 74.4,
                                 "frac": round(mm["tflops"] / 74.4, 4)},
-                   "l2": "flushed between steps (256 MiB write)"}
+                   "l2": "flushed between steps (256 MiB write)", "clocks": mm["clocks"]}
         mm_line["e2e"] = matmul_e2e_leg(3)
-        if d.n == 1:
-            mm_line["cpu_baseline"] = cpu_matmul()
         line.setdefault("matmul", {})["c2_f32"] = mm_line
-    if args.workload in ("all", "c5"):
-        c5 = c5_leg(d.n)
+    # CPU baselines last: their all-core OpenMP runs heat the host and slow
+    # the TCP-bound C5 leg if they run before it
+    if d.n == 1:
+        line["cpu_baseline"] = cpu_lut(mode)
+        if mm is not None:
+            line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
+    if c5 is not None:
         if d.n == 1:
             c5["cpu_baseline"] = cpu_c5()
         line["c5"] = c5

@@ -1,17 +1,8 @@
-cat > /tmp/one_mm.py <<'P'
-import sys, torch
-sys.path.insert(0, ".")
-from paper_1505_05655_b200 import device as D
-for s in (8192, 32768):
-    A = D.synth_matrix(1, 1, s, s); B = D.synth_matrix(1, 2, s, s); Cm = torch.empty(s, s, device="cuda")
-    ws = D.matmul_workspace(2, s, s, s)
-    D.matmul(2, A, B, Cm, ws); torch.cuda.synchronize()
-    del A, B, Cm, ws; torch.cuda.empty_cache()
+timeout 1500 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; tail -c 200 gpurun_out/bench_full.err
+python - <<'P'
+import json
+d=json.loads(open('gpurun_out/bench_full.json').read().strip().splitlines()[-1])
+print(json.dumps({k:d.get(k) for k in ('value','ms_per_step','gpu_launches')}), json.dumps(d['e2e'])[:300], d['roofline']['frac'])
+m=d['matmul']; print('C4', m['value'], m['roofline']['frac'], m['clocks']); c2=m['c2_f32']; print('C2', c2['value'], c2['clocks'], c2['e2e']['value'], c2['cpu_baseline']['value'])
+print('C5', d['c5']['chains_per_s'], d['c5']['cpu_baseline']['chains_per_s'])
 P
-timeout 600 python -m pytest tests/test_matmul_gpu.py tests/test_executor.py -x -q -m gpu > gpurun_out/t_mm.log 2>&1; tail -3 gpurun_out/t_mm.log
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'prep|gemm' --csv python /tmp/one_mm.py 2>/dev/null | grep -v "^==" | python -c "
-import csv,sys
-for r in csv.reader(sys.stdin):
-    if len(r)>10: print(r[4][:40], r[-3], r[-2], r[-1])
-"
-for rep in 1 2; do timeout 300 python tools/c4_ab.py 2sm 2>/dev/null | cut -c1-200; done
