@@ -614,10 +614,11 @@ def run_b200(args) -> None:
             "ms_per_step": round(c4["ms_max"], 3), "scaling": "strong",
             "includes": "f32->bf16 operand preparation + GEMM + f32 C write",
             "tolerance": "|c-c_ref| <= 1e-5 * sum|a||b| vs f64 oracle on bf16-rounded operands (tests/test_matmul_gpu.py)",
-            "roofline": {"bound": "tensor", "kernel": "gemm::gemm_kernel<bf16>", "achieved": round(ach, 1),
+            "roofline": {"bound": "tensor", "kernel": "gemm::gemm2_kernel<bf16> (+ prep_a/prep_bt)",
+                         "achieved": round(ach, 1),
                          "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                          "peak_source": f"{pk['source']} bf16 cuBLAS, sustained (kernel timed in a long loop)",
-                         "traffic": tr.get("gemm_kernel", {}).get("bytes_per_launch")},
+                         "traffic": tr.get("gemm2_kernel", {}).get("bytes_per_launch")},
             "clocks": c4["clocks"]}
     if mm is not None:
         mm_line = {"workload": "C2: MATMUL prec=f32 (SIMT, reference precision), 4096^3",
