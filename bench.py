@@ -254,8 +254,32 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     # here; the oracle check of this exact band runs in the cpu leg).
     dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
     st = D.read_stats(stats)
+    gather_ms = gather_leg(d, out) if d.pg is not None else None
     return {"ms": ms, "hist_ms": hist_ms, "exch_ms": exch_ms, "band_px": n, "digest": dig,
-            "stats": st, "clocks": clk.summary()}
+            "stats": st, "clocks": clk.summary(), "gather_ms": gather_ms}
+
+
+def gather_leg(d: Dist, out, reps: int = 3) -> float:
+    """N>1: the final gather of the corrected bands to rank 0 (NCCL over
+    NVLink; paper_1505_05655_b200.shard.gather_bands), timed on its own --
+    SURVEY.md §8e: sharded-compute scaling is reported separately from the
+    gather.  Max over ranks of the mean of `reps` gathers."""
+    import torch
+    from paper_1505_05655_b200.shard import gather_bands
+    rows_per = [band(ROWS, d.n, r)[1] for r in range(d.n)]
+    nccl = d.pg.get_backend() == "nccl"
+    src = out if nccl else out.cpu()
+    gather_bands(d.pg, src, rows_per, COLS)  # warm-up (communicator buffers)
+    d.barrier()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(reps):
+        full = gather_bands(d.pg, src, rows_per, COLS)
+        torch.cuda.synchronize()
+        del full
+    ms = (time.perf_counter() - t) * 1e3 / reps
+    d.barrier()
+    return ms
 
 
 def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int = 1) -> dict:
@@ -537,6 +561,7 @@ def run_b200(args) -> None:
     ms = d.max(lut["ms"])
     exch_ms = d.max(lut["exch_ms"]) if lut["exch_ms"] is not None else None
     hist_ms = d.max(lut["hist_ms"])
+    gather_ms = d.max(lut["gather_ms"]) if lut["gather_ms"] is not None else None
     mm = c4 = None
     if args.workload in ("all", "matmul"):
         torch.cuda.empty_cache()
@@ -574,6 +599,12 @@ def run_b200(args) -> None:
                                  "algorithmic_bytes": 6 * band_px}}}
     if exch_ms is not None:
         roof["kernels"]["histogram_all_reduce"] = {"ms": round(exch_ms, 4), "bytes": 262144}
+    gather = None
+    if gather_ms is not None:
+        gather = {"ms": round(gather_ms, 3), "bytes": 2 * ROWS * COLS,
+                  "what": "corrected bands gathered to rank 0 (torch.distributed.gather, "
+                          + ("gloo via host: GPCX_BENCH_ONE_GPU test mode" if Dist.one_gpu else "NCCL")
+                          + "); not in `value` -- the output stays sharded in HBM there"}
     launches = 1 if exch_ms is None else 2
     line = {"metric": METRIC, "value": round(value, 2), "unit": "Gpixel/s", "n_gpus": d.n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
@@ -586,6 +617,8 @@ def run_b200(args) -> None:
             # per step: fused_kernel once at N=1; count + build/apply launches at N>1
             "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": lut["clocks"]}
+    if gather is not None:
+        line["gather"] = gather
     c5 = None
     if args.workload in ("all", "c5"):
         time.sleep(2)  # let the clock recover from the C4 leg

@@ -59,8 +59,9 @@ def gather_bands(dist, band_out, rows_per_rank: list[int], cols: int):
     per = max(rows_per_rank)
     padded = torch.zeros(per * cols, dtype=band_out.dtype, device=band_out.device)
     padded[: band_out.numel()] = band_out.reshape(-1)
-    parts = [torch.empty_like(padded) for _ in range(world)] if dist.get_rank() == 0 else None
-    dist.gather(padded, parts, dst=0)
+    wire = padded.view(torch.uint8)  # bytes: every backend carries u8 (gloo has no int16)
+    parts = [torch.empty_like(wire) for _ in range(world)] if dist.get_rank() == 0 else None
+    dist.gather(wire, parts, dst=0)
     if dist.get_rank() != 0:
         return None
-    return torch.cat([p[: r * cols] for p, r in zip(parts, rows_per_rank)])
+    return torch.cat([p.view(band_out.dtype)[: r * cols] for p, r in zip(parts, rows_per_rank)])

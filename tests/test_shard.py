@@ -51,8 +51,8 @@ def _worker(rank, world, port, rows, cols, mode, q):
     def lut_from_hist(h):
         return O.lut_from_hist(h.numpy().astype(np.uint64), mode)
 
-    def apply(lut, b):
-        return torch.from_numpy(lut[b.numpy()].astype(np.int64))
+    def apply(lut, b):  # int16 carrier, like the device path (gather moves bytes)
+        return torch.from_numpy(lut[b.numpy()].astype(np.uint16).view(np.int16))
 
     out, lut, stats = ShardedLut(dist, hist, lut_from_hist, apply).run(img)
     full = gather_bands(dist, out, [nr_ for _, nr_ in bands(rows, world)], cols)
