@@ -33,8 +33,29 @@ def main():
         out = torch.empty_like(img)
         lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
         D.lut_correct(img, out, 0, lut, stats, ws)
+        D.lut_apply(lut, img, out)  # LUT_APPLY's kernel on the same scene
         torch.cuda.synchronize()
         del img, out
+    if "sgemm" in args.what:  # config C2: FP32 SIMT 4096^3
+        A = D.synth_matrix(1, 1, 4096, 4096)
+        B = D.synth_matrix(1, 2, 4096, 4096)
+        Cm = torch.empty(4096, 4096, device="cuda")
+        D.matmul(0, A, B, Cm)
+        torch.cuda.synchronize()
+    if "demosaic" in args.what:  # BAYER_BILINEAR / BAYER_GRADIENT at 16384^2
+        img = D.synth_image(1, 3, 16384, 16384)
+        for grad in (False, True):
+            D.demosaic(grad, 0, img, 16384, 16384)
+        torch.cuda.synchronize()
+    if "c4" in args.what.split(","):  # config C4: one 32768^3 bf16 MATMUL
+        A = D.synth_matrix(1, 1, 32768, 32768)
+        B = D.synth_matrix(1, 2, 32768, 32768)
+        Cm = torch.empty(32768, 32768, device="cuda")
+        ws = D.matmul_workspace(2, 32768, 32768, 32768)
+        D.matmul(2, A, B, Cm, ws)
+        torch.cuda.synchronize()
+        print("done")
+        return
     if args.what == "longk2":  # one long-K GEMM with the caller's GPCX_TC_* environment
         A = D.synth_matrix(1, 1, 8192, 32768)
         B = D.synth_matrix(1, 2, 32768, 8192)
@@ -58,7 +79,7 @@ def main():
             torch.cuda.synchronize()
         print("done")
         return
-    if "mm" in args.what:
+    if "mm" in args.what.split(","):
         s = args.mm
         A = D.synth_matrix(1, 1, s, s)
         B = D.synth_matrix(1, 2, s, s)
