@@ -1,3 +1,3 @@
-ncu --set full --import-source on --clock-control none -k regex:'fused_kernel|apply_kernel' -c 3 -o gpurun_out/prof_lut -f python tools/prof_target.py --what c1,lut > gpurun_out/ncu1.log 2>&1; tail -1 gpurun_out/ncu1.log
-ncu --set full --import-source on --clock-control none -k regex:'sgemm|demosaic|prep_|gemm2' -c 8 -o gpurun_out/prof_mm -f python tools/prof_target.py --what sgemm,demosaic,mm --mm 8192 > gpurun_out/ncu2.log 2>&1; tail -1 gpurun_out/ncu2.log
-ncu --set full --clock-control none -k regex:'gemm2' -c 1 -o gpurun_out/prof_c4 -f python tools/prof_target.py --what c4 > gpurun_out/ncu3.log 2>&1; tail -1 gpurun_out/ncu3.log
+timeout 600 python -m pytest tests/test_demosaic.py -x -q -m gpu > gpurun_out/t_dm.log 2>&1; tail -2 gpurun_out/t_dm.log
+timeout 300 python tools/demosaic_micro.py 2>&1 | tail -8
+timeout 600 compute-sanitizer --tool racecheck python -m pytest tests/test_demosaic.py -x -q -m gpu -k "ragged or phase" > gpurun_out/race_dm.txt 2>&1; tail -2 gpurun_out/race_dm.txt
