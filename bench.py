@@ -430,10 +430,10 @@ C5_REQUESTS = 64
 C5_CPU_SAMPLE = 16  # chains timed on the reference CPU server (bounded sample)
 
 
-def c5_inputs() -> tuple[list[bytes], bytes]:
+def c5_inputs(count: int = C5_REQUESTS) -> tuple[list[bytes], bytes]:
     from paper_1505_05655_b200 import device as D
     imgs = [D.synth_image(0, SEED + i, C5_IMG, C5_IMG).cpu().numpy().view(np.uint16).tobytes()
-            for i in range(C5_REQUESTS)]
+            for i in range(count)]
     B = D.synth_matrix(1, SEED_B, C5_MM, C5_MM).cpu().numpy().tobytes()
     return imgs, B
 
@@ -498,6 +498,41 @@ def c5_leg(n_gpus: int) -> dict:
     return res
 
 
+def c1_run(port: int, img: bytes, reps: int, warmup: int = 2) -> dict:
+    """Config C1: ONE client request at a time -- LUT_CORRECT of a 4096^2
+    u16 image over loopback TCP (260-byte header + 32 MiB up, 32 MiB down),
+    latency per request; the native client (gpcx_client_submit)."""
+    from paper_1505_05655_b200.client import submit_native as submit
+    out = np.empty(C5_IMG * C5_IMG, dtype=np.uint16)
+    dims = f"rows={C5_IMG},cols={C5_IMG},mode=equalize"
+    ts = []
+    for i in range(warmup + reps):
+        t = time.perf_counter()
+        r = submit("127.0.0.1", port, "LUT_CORRECT", dims, [img], output_name="c1.raw",
+                   out=out.view(np.uint8))
+        assert r.ok, r.status
+        if i >= warmup:
+            ts.append(time.perf_counter() - t)
+    ms = statistics.median(ts) * 1e3
+    return {"ms_per_request": round(ms, 3), "Gpixel/s": round(C5_IMG * C5_IMG / ms / 1e6, 3),
+            "requests": reps, "digest": int(np.frombuffer(out.tobytes(), dtype=np.uint64).sum(
+                dtype=np.uint64))}
+
+
+def c1_leg(n_gpus: int) -> dict:
+    import paper_1505_05655_b200 as G
+    imgs, _ = c5_inputs(count=1)
+    G.init(bound_devices(n_gpus))
+    try:
+        with G.Server(max_tasks=0) as srv:
+            res = c1_run(srv.port, imgs[0], reps=20)
+    finally:
+        G.init([0])
+    res["workload"] = ("C1: one LUT_CORRECT request (4096^2 u16, equalize) at a time through the "
+                       "B200 server, loopback TCP, median latency")
+    return res
+
+
 # -------------------------------------------------------------- CPU legs ---
 
 def cpu_c5() -> dict:
@@ -513,6 +548,18 @@ def cpu_c5() -> dict:
                           "clients, through the reference server "
                           "(oracle/_ref: reference server + restated CPU kernels)"})
     return res
+
+def cpu_c1() -> dict:
+    """C1 against the reference server (its TCP / dispatch code, the restated
+    LUT_CORRECT on all host cores)."""
+    from oracle import oracle as O
+    imgs, _ = c5_inputs(count=1)
+    with O.RefServer(max_tasks=0) as rs:
+        res = c1_run(rs.port, imgs[0], reps=5, warmup=1)
+    res.update({"kind": "port", "cores": O.max_threads(),
+                "sample": "5 sequential requests after 1 warm-up, same image and client"})
+    return res
+
 
 def cpu_lut(mode: int, sample_rows: int = 4096, reps: int = 3) -> dict:
     """The restated oracle (kind "port") on a row-band sample of the C3
@@ -619,10 +666,11 @@ def run_b200(args) -> None:
             "clocks": lut["clocks"]}
     if gather is not None:
         line["gather"] = gather
-    c5 = None
+    c5 = c1 = None
     if args.workload in ("all", "c5"):
         time.sleep(2)  # let the clock recover from the C4 leg
         c5 = c5_leg(d.n)
+        c1 = c1_leg(d.n)
     e2e_steps = max(4, min(args.steps, 8))
     e2e1 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=1)
     e2e2 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=2)
@@ -673,6 +721,13 @@ def run_b200(args) -> None:
         if d.n == 1:
             c5["cpu_baseline"] = cpu_c5()
         line["c5"] = c5
+    if c1 is not None:
+        if d.n == 1:
+            ref = cpu_c1()
+            c1["cpu_baseline"] = ref
+            c1["output_identical_to_reference_server"] = ref.pop("digest") == c1["digest"]
+        c1.pop("digest")
+        line["c1"] = c1
     print(json.dumps(line), flush=True)
 
 

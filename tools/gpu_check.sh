@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests/test_demosaic.py -x -q -m gpu > gpurun_out/t_dm.log 2>&1; tail -2 gpurun_out/t_dm.log
-timeout 300 python tools/demosaic_micro.py 2>&1 | tail -8
-timeout 600 compute-sanitizer --tool racecheck python -m pytest tests/test_demosaic.py -x -q -m gpu -k "ragged or phase" > gpurun_out/race_dm.txt 2>&1; tail -2 gpurun_out/race_dm.txt
+timeout 900 python bench.py --workload c5 --steps 5 --warmup 3 > gpurun_out/b_c5.json 2> gpurun_out/b_c5.err; tail -c 300 gpurun_out/b_c5.err
+python -c "
+import json;d=json.loads(open('gpurun_out/b_c5.json').read().strip().splitlines()[-1]);print(json.dumps(d.get('c1'))); print(d['c5']['chains_per_s'])"
