@@ -1,3 +1,1 @@
-timeout 900 python bench.py --workload c5 --steps 5 --warmup 3 > gpurun_out/b_c5.json 2> gpurun_out/b_c5.err; tail -c 300 gpurun_out/b_c5.err
-python -c "
-import json;d=json.loads(open('gpurun_out/b_c5.json').read().strip().splitlines()[-1]);print(json.dumps(d.get('c1'))); print(d['c5']['chains_per_s'])"
+timeout 900 python -m pytest tests/test_matmul_gpu.py -x -q -m gpu -k "c4_full" --durations=3 > gpurun_out/t_c4.log 2>&1; tail -6 gpurun_out/t_c4.log
