@@ -7,7 +7,8 @@
 // plain fp32 FFMA accumulation in a fixed, K-ascending order per output, so
 // results are deterministic and identical for any block-row sharding.
 //
-// Tiling: 128x128 CTA tile, BK = 8 or 16, 256 threads each owning an 8x8
+// sgemm2_kernel (aligned shapes): cp.async multistage, see below.
+// sgemm_kernel (any shape): 128x128 CTA tile, BK = 8 or 16, 256 threads each owning an 8x8
 // block (2x2 quads of 4x4 so the 128-bit smem reads stay conflict-free), A
 // staged transposed, double-buffered smem with register prefetch of the
 // next tile.  Variant <BK, min CTAs/SM> is picked per launch
@@ -136,6 +137,127 @@ __global__ void __launch_bounds__(THREADS, MINB)
   }
 }
 
+// ---- cp.async multistage variant (aligned shapes) ---------------------
+// 128 x 64 CTA tile, 128 threads, 8 x 8 outputs per thread, BK = 16, a
+// 3-stage cp.async ring: both operand tiles are copied global -> smem
+// without passing through registers, so the K loop issues only LDS + FFMA.
+// A stays row-major in smem (row pitch 20 floats): a thread reads its 8
+// rows' 4 consecutive k as one LDS.128 each; thread (tx, ty) owns rows
+// ty + 16 i (a warp's 4 ty values hit 4 distinct bank groups) and columns
+// 4 tx + {0..3}, 32 + 4 tx + {0..3}.  Per 4 k: 16 LDS.128 for 256 FFMA.
+// Each output is still fma-accumulated over k in ascending order, so the
+// result is bitwise identical to sgemm_kernel's.
+constexpr int BM2 = 128, BN2 = 64, THREADS2 = 128;
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<std::uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
+template <int BK2, int STAGES2>
+constexpr int sgemm2_smem() {
+  return STAGES2 * (BM2 * (BK2 + 4) + BK2 * BN2) * 4;
+}
+
+template <int BK2, int STAGES2, int MINB>
+__global__ void __launch_bounds__(THREADS2, MINB)
+    sgemm2_kernel(int k, const float* __restrict__ A, std::uint64_t lda,
+                  const float* __restrict__ B, std::uint64_t ldb, float* __restrict__ C,
+                  std::uint64_t ldc) {
+  constexpr int APITCH = BK2 + 4;  // floats
+  extern __shared__ __align__(16) float smem2[];
+  float (*As)[BM2 * APITCH] = reinterpret_cast<float (*)[BM2 * APITCH]>(smem2);
+  float (*Bs)[BK2 * BN2] = reinterpret_cast<float (*)[BK2 * BN2]>(smem2 + STAGES2 * BM2 * APITCH);
+  const int tid = threadIdx.x;
+  const int tx = tid & 7, ty = tid >> 3;
+  const int m0 = blockIdx.y * BM2, n0 = blockIdx.x * BN2;
+  const float* Ablk = A + static_cast<std::uint64_t>(m0) * lda;
+  const float* Bblk = B + n0;
+
+  auto issue = [&](int stage, int k0) {
+#pragma unroll
+    for (int i = 0; i < BK2 / 4; ++i) {  // A: 128 rows x BK2/4 chunks of 16 B
+      const int c = tid + THREADS2 * i;
+      const int row = c / (BK2 / 4), q = c % (BK2 / 4);
+      cp16(&As[stage][row * APITCH + 4 * q], Ablk + static_cast<std::uint64_t>(row) * lda + k0 + 4 * q);
+    }
+#pragma unroll
+    for (int i = 0; i < BK2 / 8; ++i) {  // B: BK2 rows x 16 chunks of 16 B
+      const int c = tid + THREADS2 * i;
+      const int kr = c >> 4, q = c & 15;
+      cp16(&Bs[stage][kr * BN2 + 4 * q], Bblk + static_cast<std::uint64_t>(k0 + kr) * ldb + 4 * q);
+    }
+  };
+
+  // acc[i][p] = outputs (row i, columns 2p, 2p+1 of the thread's 8):
+  // FFMA2 (Blackwell packed fp32x2 FMA, IEEE fma per lane -> the same bits
+  // as two fmaf) with a[i] broadcast: half the FMA instructions and half
+  // the accumulator register reads per flop of a scalar FFMA loop.
+  float2 acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) acc[i][p] = make_float2(0.f, 0.f);
+
+  const int ktiles = k / BK2;
+#pragma unroll
+  for (int st = 0; st < STAGES2 - 1; ++st) {
+    if (st < ktiles) issue(st, st * BK2);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int t = 0; t < ktiles; ++t) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES2 - 2) : "memory");
+    __syncthreads();  // tile t visible; stage (t - 1) % S free to refill
+    const int nt = t + STAGES2 - 1;
+    if (nt < ktiles) issue(nt % STAGES2, nt * BK2);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* as = As[t % STAGES2];
+    const float* bs = Bs[t % STAGES2];
+#pragma unroll
+    for (int kq = 0; kq < BK2; kq += 4) {
+      float a[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(&as[(ty + 16 * i) * APITCH + kq]);
+        a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 b0 = *reinterpret_cast<const float4*>(&bs[(kq + kk) * BN2 + 4 * tx]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&bs[(kq + kk) * BN2 + 32 + 4 * tx]);
+        const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                             make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 ai = make_float2(a[i][kk], a[i][kk]);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) acc[i][p] = __ffma2_rn(ai, b[p], acc[i][p]);
+        }
+      }
+    }
+  }
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float* crow = C + static_cast<std::uint64_t>(m0 + ty + 16 * i) * ldc + n0;
+    *reinterpret_cast<float4*>(crow + 4 * tx) =
+        make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+    *reinterpret_cast<float4*>(crow + 32 + 4 * tx) =
+        make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+  }
+}
+
+bool sgemm2_fits(std::uint64_t m, std::uint64_t n, std::uint64_t k, const float* A,
+                 std::uint64_t lda, const float* B, std::uint64_t ldb, const float* C,
+                 std::uint64_t ldc) {
+  return m % BM2 == 0 && n % BN2 == 0 && k % 32 == 0 && lda % 4 == 0 && ldb % 4 == 0 &&
+         ldc % 4 == 0 && (m / BM2) <= 65535 &&
+         ((reinterpret_cast<std::uintptr_t>(A) | reinterpret_cast<std::uintptr_t>(B) |
+           reinterpret_cast<std::uintptr_t>(C)) & 15u) == 0;
+}
+
 template <int BK, int MINB>
 void launch_variant(std::uint64_t m, std::uint64_t n, std::uint64_t k, const float* A,
                     std::uint64_t lda, const float* B, std::uint64_t ldb, float* C,
@@ -171,9 +293,24 @@ void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
     return;
   }
   const char* v = std::getenv("GPCX_SGEMM");
-  // Default BK=8 with 2 CTAs/SM: 49.6 / 50.8 TFLOP/s at 4096^3 / 8192^3 vs
-  // 47.4 / 48.5 for BK=16, 1 CTA/SM (B200, tools/mm_micro.py).
-  const std::string variant = v != nullptr ? v : "8x2";
+  const std::string variant = v != nullptr ? v : "";
+  if ((variant.empty() || variant[0] == 'c') && sgemm2_fits(m, n, k, A, lda, B, ldb, C, ldc)) {
+    const dim3 grid(static_cast<unsigned>(n / BN2), static_cast<unsigned>(m / BM2));
+    auto go = [&](auto kernel, int smem) {
+      GPCX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kernel<<<grid, THREADS2, smem, stream>>>(static_cast<int>(k), A, lda, B, ldb, C, ldc);
+    };
+    // GPCX_SGEMM=c16x3 | c16x4 | c32x3 (BK x stages) for A/B runs
+    if (variant == "c16x4") go(sgemm2_kernel<16, 4, 2>, sgemm2_smem<16, 4>());
+    else if (variant == "c32x3") go(sgemm2_kernel<32, 3, 2>, sgemm2_smem<32, 3>());
+    else if (variant == "c16x3b3") go(sgemm2_kernel<16, 3, 3>, sgemm2_smem<16, 3>());
+    else go(sgemm2_kernel<16, 3, 2>, sgemm2_smem<16, 3>());
+    GPCX_LAUNCH_CHECK();
+    return;
+  }
+  // Register-staged kernel for ragged / unaligned shapes (and A/B runs):
+  // BK=8 with 2 CTAs/SM: 49.6 / 50.8 TFLOP/s at 4096^3 / 8192^3 vs 47.4 /
+  // 48.5 for BK=16, 1 CTA/SM (B200, tools/mm_micro.py).
   if (variant == "16x1") launch_variant<16, 1>(m, n, k, A, lda, B, ldb, C, ldc, stream);
   else if (variant == "16x2") launch_variant<16, 2>(m, n, k, A, lda, B, ldb, C, ldc, stream);
   else launch_variant<8, 2>(m, n, k, A, lda, B, ldb, C, ldc, stream);
