@@ -234,11 +234,13 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
     s.a.ensure(std::max<std::uint64_t>(b.nrows * p.k * 4, 4));
     s.b.ensure(std::max<std::uint64_t>(p.k * row_bytes, 4));
     s.c.ensure(std::max<std::uint64_t>(b.nrows * p.n * 4, 4));
+    // A before B: a request payload (A || B) may still be arriving
+    // (rt::Arrival), and A lands first.
+    rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
     rt::h2d(s, s.b.as<std::uint8_t>() + ks[i] * row_bytes,
             reinterpret_cast<const std::uint8_t*>(B) + ks[i] * row_bytes,
             (ks[i + 1] - ks[i]) * row_bytes);
     GPCX_CUDA(cudaEventRecord(s.ready, s.stream));
-    rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
   });
 
   for_each_band(G, [&](std::size_t i) {

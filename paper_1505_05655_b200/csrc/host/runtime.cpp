@@ -276,8 +276,78 @@ bool is_pinned(const void* p) {
   return attr.type == cudaMemoryTypeHost;
 }
 
+namespace {
+struct ArrivalRegistry {
+  std::mutex mu;
+  std::vector<Arrival*> live;
+};
+ArrivalRegistry& arrivals() {
+  static ArrivalRegistry* r = new ArrivalRegistry();
+  return *r;
+}
+Arrival* find_arrival(const void* p) {
+  ArrivalRegistry& r = arrivals();
+  std::lock_guard<std::mutex> lock(r.mu);
+  const auto* b = static_cast<const std::uint8_t*>(p);
+  for (Arrival* a : r.live)
+    if (b >= a->base() && b < a->base() + a->size()) return a;
+  return nullptr;
+}
+}  // namespace
+
+Arrival::Arrival(const void* base, std::uint64_t len)
+    : base_(static_cast<const std::uint8_t*>(base)), len_(len) {
+  ArrivalRegistry& r = arrivals();
+  std::lock_guard<std::mutex> lock(r.mu);
+  r.live.push_back(this);
+}
+
+Arrival::~Arrival() {
+  ArrivalRegistry& r = arrivals();
+  std::lock_guard<std::mutex> lock(r.mu);
+  for (std::size_t i = 0; i < r.live.size(); ++i) {
+    if (r.live[i] == this) {
+      r.live.erase(r.live.begin() + static_cast<std::ptrdiff_t>(i));
+      break;
+    }
+  }
+}
+
+void Arrival::advance(std::uint64_t got) {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    got_ = got;
+  }
+  cv_.notify_all();
+}
+
+void Arrival::fail() {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    failed_ = true;
+  }
+  cv_.notify_all();
+}
+
+void Arrival::wait_for(std::uint64_t upto) {
+  std::unique_lock<std::mutex> lock(mu_);
+  cv_.wait(lock, [&] { return failed_ || got_ >= upto; });
+  if (got_ < upto) gpcx::fail(Errc::Truncated, "request payload ended early");
+}
+
 void h2d(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
   if (bytes == 0) return;
+  if (Arrival* a = find_arrival(src)) {  // payload still arriving: chunk as it lands
+    const std::uint64_t start = static_cast<std::uint64_t>(static_cast<const std::uint8_t*>(src) - a->base());
+    const auto* in = static_cast<const std::uint8_t*>(src);
+    auto* out = static_cast<std::uint8_t*>(dst);
+    for (std::uint64_t off = 0; off < bytes; off += kArrivalChunk) {
+      const std::uint64_t len = std::min(kArrivalChunk, bytes - off);
+      a->wait_for(start + off + len);
+      GPCX_CUDA(cudaMemcpyAsync(out + off, in + off, len, cudaMemcpyHostToDevice, s.stream));
+    }
+    return;
+  }
   if (is_pinned(src)) {
     GPCX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s.stream));
     return;

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -109,6 +110,32 @@ class Runtime {
   std::vector<Pool> pools_;
   std::atomic<unsigned> rr_{0};
 };
+
+// A request payload still arriving from the network into a pinned buffer
+// (SURVEY.md §8f row 2).  While it is registered, h2d() of a range inside
+// it copies chunk by chunk as the bytes land, so the DMA to HBM overlaps
+// the receive instead of starting after the last byte.
+class Arrival {
+ public:
+  Arrival(const void* base, std::uint64_t len);
+  ~Arrival();
+  Arrival(const Arrival&) = delete;
+  Arrival& operator=(const Arrival&) = delete;
+  void advance(std::uint64_t got);  // bytes [0, got) are in place
+  void fail();                      // the receive failed: waiters throw Truncated
+  void wait_for(std::uint64_t upto);
+  const std::uint8_t* base() const { return base_; }
+  std::uint64_t size() const { return len_; }
+
+ private:
+  const std::uint8_t* base_;
+  std::uint64_t len_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::uint64_t got_ = 0;
+  bool failed_ = false;
+};
+inline constexpr std::uint64_t kArrivalChunk = 4ull << 20;
 
 // Host -> device copy on the slot stream.  Pinned sources go straight to the
 // DMA engine; pageable sources are staged chunk-wise (returns once the last

@@ -159,3 +159,46 @@ def test_native_client_round_trips_errors_like_reference_client(server, refl):
     with pytest.raises(G.GpcxError) as e:
         submit_native("127.0.0.1", 1, "NOPE", "", [], 0)
     assert e.value.code == "ConnectFailed"
+
+
+def test_large_payload_cut_short_drops_connection(server):
+    """A >= 8 MiB payload is handed to the task while it arrives; if the
+    client stops early the request is dropped (no response), like the
+    reference's read_exact failure, and the server keeps serving."""
+    with socket.create_connection(("127.0.0.1", server.port), timeout=10) as s:
+        s.sendall(W.header("LUT_CORRECT", "rows=2048,cols=4096", has_payload=True))
+        s.sendall(b"\0" * (5 << 20))  # 5 of 16 MiB, then half-close
+        s.shutdown(socket.SHUT_WR)
+        t0 = time.time()
+        data = s.recv(4096)
+        assert data == b"" and time.time() - t0 < 10
+    with socket.create_connection(("127.0.0.1", server.port), timeout=10) as s:
+        s.sendall(W.header("NOPE", "", name="after"))
+        assert W.parse_response(s.recv(4096))["status"] == "ERR:UNKNOWN_TASK"
+
+
+@pytest.mark.gpu
+def test_large_requests_overlap_receive_and_match(gpu, server):
+    """>= 8 MiB payloads take the receive-overlapped path (rt::Arrival):
+    LUT_CORRECT 4096^2 (32 MiB) and MATMUL 1536^3 f32 (18 MiB) served
+    results equal the oracle."""
+    from oracle import oracle as O
+    from paper_1505_05655_b200.client import submit_native
+    img = O.synth_image(O.IMG_RAMP12, 77, 4096, 4096)
+    out = np.empty(img.size, dtype=np.uint16)
+    r = submit_native("127.0.0.1", server.port, "LUT_CORRECT", "rows=4096,cols=4096",
+                      [img], img.nbytes, "big.raw", out=out.view(np.uint8))
+    assert r.ok, r.status
+    ref_out, _, _ = O.lut_correct(img, O.LUT_EQUALIZE)
+    assert np.array_equal(out, ref_out)
+    n = 1536
+    A = O.synth_matrix(O.MAT_UNIFORM32, 5, n, n)
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(5), n, n)
+    cm = np.empty(n * n, dtype=np.float32)
+    r = submit_native("127.0.0.1", server.port, "MATMUL", f"m={n},k={n},n={n}", [A, B],
+                      cm.nbytes, "c.f32", out=cm.view(np.uint8))
+    assert r.ok, r.status
+    rows = np.arange(0, n, 97).astype(np.uint64)
+    Cref, ab = O.matmul_f64(A, B, rows)
+    got = cm.reshape(n, n)[rows.astype(np.int64)].astype(np.float64)
+    assert np.all(np.abs(got - Cref) <= 1e-5 * ab + 1e-30)
