@@ -363,9 +363,24 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
     d.barrier()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
-    del A, B, Cm, ws
+    del A, B, ws
+    gather_ms = None
+    if d.pg is not None:  # the C bands to rank 0, timed apart from the compute
+        from paper_1505_05655_b200.shard import gather_bands
+        rows_per = [band(MM4, d.n, r)[1] for r in range(d.n)]
+        src = Cm if d.pg.get_backend() == "nccl" else Cm.cpu()
+        gather_bands(d.pg, src, rows_per, MM4)
+        d.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        full = gather_bands(d.pg, src, rows_per, MM4)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - t) * 1e3
+        del full, src
+        d.barrier()
+    del Cm
     torch.cuda.empty_cache()
-    return {"ms": ms, "rows": nr, "clocks": clk.summary()}
+    return {"ms": ms, "rows": nr, "clocks": clk.summary(), "gather_ms": gather_ms}
 
 
 def matmul_device_leg(steps: int, warmup: int) -> dict:
@@ -619,6 +634,8 @@ def run_b200(args) -> None:
         d.barrier()
         c4 = matmul_c4_leg(d, max(2, min(args.steps, 5)), 1)
         c4["ms_max"] = d.max(c4["ms"])
+        if c4["gather_ms"] is not None:
+            c4["gather_ms"] = d.max(c4["gather_ms"])
     d.barrier()
     if d.rank != 0:
         d.close()
@@ -701,6 +718,9 @@ def run_b200(args) -> None:
                          "peak_source": f"{pk['source']} bf16 cuBLAS, sustained (kernel timed in a long loop)",
                          "traffic": tr.get("gemm2_kernel", {}).get("bytes_per_launch")},
             "clocks": c4["clocks"]}
+        if c4["gather_ms"] is not None:
+            line["matmul"]["gather"] = {"ms": round(c4["gather_ms"], 3), "bytes": 4 * MM4 * MM4,
+                                        "what": "C bands (f32) gathered to rank 0, not in `value`"}
     if mm is not None:
         mm_line = {"workload": "C2: MATMUL prec=f32 (SIMT, reference precision), 4096^3",
                    "value": round(mm["tflops"], 2),
