@@ -9,6 +9,10 @@
 //   4 a quarter of the pixels to red.global
 //   5 all pixels red.global (per-CTA L2 histogram)
 //   6 __match_any_sync aggregation, one red.shared per distinct value
+//   7 red.shared, packed u8 quads (64 KiB: 4 bins per word)
+//   8 / 9  u8 quads, 2 / 3 replicas (warp w uses replica w % R)
+//   10 atom (returning) u16 pairs + the wrap check (the product's count_one)
+//   11 atom u8 quads x2 replicas + wrap check
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -49,7 +53,7 @@ template <int MODE>
 __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh) {
   extern __shared__ uint4 sm[];
   uint32_t* bins = (uint32_t*)sm;
-  for (int i = threadIdx.x; i < 8192; i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < (MODE == 9 ? 12288 : 8192); i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* mine = gh + (uint64_t)blockIdx.x * 65536;
@@ -63,6 +67,18 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
     else if (MODE == 3) { if (slot & 1) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 4) { if ((slot & 3) == 3) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 5) redg(mine + v, 1);
+    else if (MODE == 7) reds(bins, v >> 2, 1u << ((v & 3) << 3));
+    else if (MODE == 8) reds(bins + ((threadIdx.x >> 5) & 1) * 16384, v >> 2, 1u << ((v & 3) << 3));
+    else if (MODE == 9) reds(bins + ((threadIdx.x >> 5) % 3) * 16384, v >> 2, 1u << ((v & 3) << 3));
+    else if (MODE == 10) {
+      const uint32_t old = atomicAdd(bins + (v >> 1), inc);
+      const uint32_t mask = (v & 1) ? 0xFFFF0000u : 0xFFFFu;
+      if ((old & mask) == mask) redg(mine + v, 65536);
+    } else if (MODE == 11) {
+      const uint32_t sh = (v & 3) << 3;
+      const uint32_t old = atomicAdd(bins + ((threadIdx.x >> 5) & 1) * 16384 + (v >> 2), 1u << sh);
+      if (((old >> sh) & 0xFFu) == 0xFFu) redg(mine + v, 256);
+    }
     else if (MODE == 6) {
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, v);
       if ((peers & ((1u << lane) - 1)) == 0) reds(bins, v >> 1, inc * __popc(peers));
@@ -88,7 +104,8 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
 
 template <int MODE>
 void run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh, int sms) {
-  cudaFuncSetAttribute(hist<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  const int smem = MODE == 9 ? 3 * 65536 : 131072;
+  cudaFuncSetAttribute(hist<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -96,7 +113,7 @@ void run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uin
   for (int r = 0; r < 6; ++r) {
     cudaMemsetAsync(gh, 0, (uint64_t)sms * 65536 * 4);
     cudaEventRecord(a);
-    hist<MODE><<<sms, 1024, 131072>>>(img, n, parts, gh);
+    hist<MODE><<<sms, 1024, smem>>>(img, n, parts, gh);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -128,6 +145,11 @@ int main() {
     run<4>("4 1/4 red.global", img, n, parts, gh, sms);
     run<5>("5 all red.global", img, n, parts, gh, sms);
     run<6>("6 match_any aggregated", img, n, parts, gh, sms);
+    run<7>("7 red.shared u8 packed", img, n, parts, gh, sms);
+    run<8>("8 red.shared u8 x2 replicas", img, n, parts, gh, sms);
+    run<9>("9 red.shared u8 x3 replicas", img, n, parts, gh, sms);
+    run<10>("10 atom u16 packed + ovf check", img, n, parts, gh, sms);
+    run<11>("11 atom u8 x2 + ovf check", img, n, parts, gh, sms);
   }
   return 0;
 }
