@@ -434,6 +434,67 @@ def matmul_e2e_leg(steps: int) -> dict:
             "d2h_bytes_per_step": nb}
 
 
+# ------------------------------------------------------------ demosaic ---
+
+DM = 16384  # BAYER_* device leg: 16384^2 u16 mosaic (512 MiB in, 1.5 GiB out > L2)
+
+
+def demosaic_leg(steps: int, warmup: int) -> dict:
+    """BAYER_BILINEAR / BAYER_GRADIENT (RGGB) on a
+    16384^2 uniform16 mosaic, device-resident, CUDA events on the launch
+    stream; 8 B/px algorithmic (2 in + 6 out), inputs + outputs > L2."""
+    import torch
+    from paper_1505_05655_b200 import device as D
+    img = D.synth_image(1, SEED, DM, DM)
+    out = torch.empty(3 * DM * DM, dtype=torch.int16, device="cuda")
+    stream = torch.cuda.current_stream()
+    res = {}
+    for name, grad in (("bilinear", False), ("gradient", True)):
+        times = []
+        with Clocks(torch.cuda.current_device()) as clk:
+            for i in range(warmup + steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                D.demosaic(grad, 0, img, DM, DM, out, stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                if i >= warmup:
+                    times.append(a.elapsed_time(b))
+        ms = sum(times) / len(times)
+        res[name] = {"ms": ms, "clocks": clk.summary()}
+    del img, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def demosaic_task_leg(reps: int = 5) -> dict:
+    """BAYER_BILINEAR through the task-level C ABI (gpcx_run) with pinned
+    host buffers at 8192^2 (128 MiB request, 384 MiB response: under the
+    1 GiB wire cap): H2D + kernel + D2H per request."""
+    import ctypes as C
+    import paper_1505_05655_b200 as G
+    n = 8192
+    nin, nout = 2 * n * n, 6 * n * n
+    pin, pout = G.lib.gpcx_pinned_alloc(nin), G.lib.gpcx_pinned_alloc(nout)
+    try:
+        img = np.ctypeslib.as_array((C.c_uint16 * (n * n)).from_address(pin))
+        img[:] = np.random.default_rng(SEED).integers(0, 1 << 16, n * n, dtype=np.uint16)
+        out = np.ctypeslib.as_array((C.c_uint8 * nout).from_address(pout))
+        times = []
+        for i in range(reps + 1):
+            t = time.perf_counter()
+            G.run("BAYER_BILINEAR", f"rows={n},cols={n}", img, out)
+            if i:
+                times.append(time.perf_counter() - t)
+    finally:
+        G.lib.gpcx_pinned_free(pin)
+        G.lib.gpcx_pinned_free(pout)
+    s = statistics.median(times)
+    return {"value": n * n / s / 1e9, "unit": "Gpixel/s", "ms": round(1e3 * s, 2),
+            "h2d_bytes_per_step": nin, "d2h_bytes_per_step": nout,
+            "path": f"gpcx_run BAYER_BILINEAR rows={n},cols={n}, pinned host buffers, median of {reps}"}
+
+
 # ------------------------------------------------------------------ C5 ---
 
 # Chain sizes: the C1 image (4096^2 u16) and the C2 product (4096^3), so each
@@ -609,6 +670,26 @@ def cpu_matmul(sample_rows: int = 64) -> dict:
 
 # ----------------------------------------------------------------- main ---
 
+def cpu_demosaic(sample_rows: int = 2048, reps: int = 3) -> dict:
+    """The REFERENCE's own demosaic (proj/src/demosaic.cpp, compiled from its
+    sources into oracle/_ref) on a row band of the bench mosaic, all host
+    cores (ExecPlan workers = nproc)."""
+    from oracle import oracle as O
+    img = np.random.default_rng(SEED).integers(0, 1 << 16, sample_rows * DM, dtype=np.uint16)
+    res = {}
+    for name, grad in (("bilinear", False), ("gradient", True)):
+        times = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            O.ref_demosaic(grad, img, sample_rows, DM, "RGGB", workers=O.max_threads())
+            times.append(time.perf_counter() - t)
+        res[name] = sample_rows * DM / statistics.median(times) / 1e9
+    return {"value": round(res["bilinear"], 4), "gradient": round(res["gradient"], 4),
+            "unit": "Gpixel/s", "cores": O.max_threads(), "kind": "reference",
+            "sample": f"BAYER_BILINEAR / BAYER_GRADIENT on a {sample_rows}x{DM} uniform16 mosaic, "
+                      f"median of {reps}: the reference's img::demosaic_* with {O.max_threads()} workers"}
+
+
 def traffic_from_profiles() -> dict:
     p = ROOT / "profiles" / "traffic.json"
     return json.loads(p.read_text()) if p.exists() else {}
@@ -636,6 +717,10 @@ def run_b200(args) -> None:
         c4["ms_max"] = d.max(c4["ms"])
         if c4["gather_ms"] is not None:
             c4["gather_ms"] = d.max(c4["gather_ms"])
+    dm = None
+    if args.workload in ("all", "demosaic") and d.rank == 0:
+        torch.cuda.empty_cache()
+        dm = demosaic_leg(max(3, min(args.steps, 10)), 3)
     d.barrier()
     if d.rank != 0:
         d.close()
@@ -731,12 +816,32 @@ def run_b200(args) -> None:
                    "l2": "flushed between steps (256 MiB write)", "clocks": mm["clocks"]}
         mm_line["e2e"] = matmul_e2e_leg(3)
         line.setdefault("matmul", {})["c2_f32"] = mm_line
+    if dm is not None:
+        kern = {}
+        for name, r in dm.items():
+            ach = 8.0 * DM * DM / (r["ms"] / 1e3) / 1e9
+            kern[name] = {"ms": round(r["ms"], 4), "value": round(DM * DM / r["ms"] / 1e6, 1),
+                          "achieved": round(ach, 1), "frac": round(ach / pk["hbm_gbs"], 4),
+                          "clocks": r["clocks"]}
+        line["demosaic"] = {
+            "workload": f"SURVEY 8f row 1: BAYER_BILINEAR / BAYER_GRADIENT (RGGB), {DM}x{DM} uniform16 "
+                        "mosaic on 1 GPU, device-resident",
+            "metric": "demosaic Gpixel/s", "value": kern["bilinear"]["value"], "unit": "Gpixel/s",
+            "roofline": {"bound": "hbm", "kernel": "demosaic::demosaic_kernel",
+                         "algorithmic_bytes_per_launch": 8 * DM * DM, "unit": "GB/s",
+                         "peak": pk["hbm_gbs"], "achieved": kern["bilinear"]["achieved"],
+                         "frac": kern["bilinear"]["frac"], "traffic": tr.get("demosaic_kernel", {}).get("bytes_per_launch")},
+            "kernels": kern, "l2": "inputs + outputs (2 GiB) larger than L2",
+            "parity": "byte-identical to the reference's img::demosaic_* and gpcref oracles (tests/test_demosaic.py)"}
+        line["demosaic"]["e2e"] = demosaic_task_leg()
     # CPU baselines last: their all-core OpenMP runs heat the host and slow
     # the TCP-bound C5 leg if they run before it
     if d.n == 1:
         line["cpu_baseline"] = cpu_lut(mode)
         if mm is not None:
             line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
+        if dm is not None:
+            line["demosaic"]["cpu_baseline"] = cpu_demosaic()
     if c5 is not None:
         if d.n == 1:
             c5["cpu_baseline"] = cpu_c5()
@@ -790,7 +895,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["all", "lut", "matmul", "c5"], default="all")
+    ap.add_argument("--workload", choices=["all", "lut", "matmul", "c5", "demosaic"], default="all")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

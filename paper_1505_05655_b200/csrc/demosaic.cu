@@ -12,17 +12,24 @@
 //   neighbours clamp to the nearest edge pixel (Accessor, demosaic.cpp:26-35),
 //   CFA phase = (row, col) shift of the RGGB tile (demosaic.cpp:15-24,151-157).
 //
-// One CTA = a 16 x 256 output tile.  The (16+2) x (256+2) input tile with a
-// 1-pixel halo is staged in smem with the edge clamp applied at load time
-// (so the stencil is branch-free): interior rows arrive as one 128-bit load
-// per lane, the interior starts at a 16-byte aligned smem column, and each
-// thread reads its 4 x 10 neighbourhood as 4 x (one 128-bit + two 16-bit)
-// smem loads, produces a 2 x 8 block and writes it as 128-bit stores to the
-// three planes (R || G || B, each rows*cols u16: the reference's
-// rgb_to_le_bytes layout).  HBM-bound: 2 B in + 6 B out per pixel.
+// One CTA = an (8 * RPT) x 256 output tile, 256 threads (8 warps x 32
+// lanes), RPT = 4 rows per thread for bilinear, 8 for gradient.  The tile
+// plus a 1-pixel halo is staged in smem with the edge clamp applied at load
+// time (so the stencil is branch-free): each warp issues all of its rows'
+// 128-bit loads (and the halo columns) before its first smem store, so a CTA
+// has its whole input tile in flight at once.  The interior starts at a
+// 16-byte aligned smem column; a thread walks down its 8 columns reading one
+// smem row (one 128-bit + two 16-bit loads) per output row, keeps a 3-row
+// window in registers, and writes each output row as three 128-bit
+// streaming stores to the planes (R || G || B, each rows*cols u16: the
+// reference's rgb_to_le_bytes layout).  Site types are compile-time: the
+// kernel is specialised on the CFA column phase, and row parity is
+// warp-uniform, so no per-pixel select between the formulas remains.
+// HBM-bound: 2 B in + 6 B out per pixel.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "cuda_util.hpp"
 #include "kernels.hpp"
@@ -31,7 +38,7 @@ namespace gpcx::demosaic {
 
 namespace {
 
-constexpr int TR = 16, TC = 256, THREADS = 256;
+constexpr int TC = 256, THREADS = 256;
 constexpr int kPad = 8;              // smem column of image column c0 (16-byte aligned)
 constexpr int SW = kPad + TC + 8;    // row stride in u16 (544 B; rows start 16-byte aligned)
 
@@ -65,27 +72,96 @@ __device__ __forceinline__ Row10 load_row(const std::uint16_t* srow, int x0) {
   return r;
 }
 
-template <bool kGradient>
-__global__ void __launch_bounds__(THREADS, 4)
+// One output row of the thread's 8 columns.  The site type of column cc is
+// compile-time (kDc = column phase, kEvenRow = row phase; col0 is a multiple
+// of 8), so each variant carries only its own arithmetic -- no per-pixel
+// select between the R/B-site and G-site formulas.
+template <bool kGradient, bool kEvenRow, int kDc>
+__device__ __forceinline__ void mosaic_row(const Row10& up, const Row10& mid, const Row10& dn,
+                                           std::uint32_t (&pr)[8], std::uint32_t (&pg)[8],
+                                           std::uint32_t (&pb)[8]) {
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) {
+    const bool even_col = ((cc + kDc) & 1) == 0;
+    const std::uint32_t s = mid.v[cc + 1];
+    const std::uint32_t n = up.v[cc + 1], so = dn.v[cc + 1];
+    const std::uint32_t w = mid.v[cc], e = mid.v[cc + 2];
+    if (kEvenRow == even_col) {  // R (even/even) or B (odd/odd) site
+      std::uint32_t g;
+      if constexpr (kGradient) {
+        const std::uint32_t dh = w > e ? w - e : e - w;
+        const std::uint32_t dv = n > so ? n - so : so - n;
+        g = dh < dv ? avg2(w, e) : (dv < dh ? avg2(n, so) : avg4(n, so, w, e));
+      } else {
+        g = avg4(n, so, w, e);
+      }
+      const std::uint32_t diag = avg4(up.v[cc], up.v[cc + 2], dn.v[cc], dn.v[cc + 2]);
+      pg[cc] = g;
+      pr[cc] = kEvenRow ? s : diag;
+      pb[cc] = kEvenRow ? diag : s;
+    } else {
+      pg[cc] = s;
+      const std::uint32_t ew = avg2(w, e), ns = avg2(n, so);
+      pr[cc] = kEvenRow ? ew : ns;  // G in a red row: R from E/W
+      pb[cc] = kEvenRow ? ns : ew;
+    }
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const std::uint32_t (&p)[8]) {
+  return make_uint4(__byte_perm(p[0], p[1], 0x5410), __byte_perm(p[2], p[3], 0x5410),
+                    __byte_perm(p[4], p[5], 0x5410), __byte_perm(p[6], p[7], 0x5410));
+}
+
+// RPT output rows per thread: a CTA covers TR = 8 * RPT rows x 256 columns.
+template <int RPT>
+constexpr int kMinBlocks = 4;
+
+template <bool kGradient, int kDc, int RPT>
+__global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
     demosaic_kernel(const std::uint16_t* __restrict__ in, std::uint16_t* __restrict__ out,
-                    int rows, int cols, int dr, int dc, int vec_ok) {
+                    int rows, int cols, int dr, int vec_ok) {
+  constexpr int TR = 8 * RPT;
   __shared__ __align__(16) std::uint16_t tile[TR + 2][SW];
   const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // Stage the tile: row i of the tile is image row clamp(r0 - 1 + i).
+  // A warp owns tile rows warp, warp + 8, warp + 16: all of its global loads
+  // (rows and halo columns) are issued before the first smem store, so they
+  // are in flight together.
+  constexpr int kRowsPerWarp = (TR + 2 + THREADS / 32 - 1) / (THREADS / 32);
   const bool full_cols = vec_ok && c0 + TC <= cols;
-  for (int i = warp; i < TR + 2; i += THREADS / 32) {
-    const int gr = min(max(r0 - 1 + i, 0), rows - 1);
-    const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr) * cols;
-    std::uint16_t* srow = tile[i];
-    if (full_cols) {
-      reinterpret_cast<uint4*>(srow + kPad)[lane] = reinterpret_cast<const uint4*>(grow + c0)[lane];
-    } else {
-      for (int c = lane; c < TC; c += 32) srow[kPad + c] = grow[min(c0 + c, cols - 1)];
+  if (full_cols) {
+    uint4 q[kRowsPerWarp];
+    std::uint32_t halo[kRowsPerWarp];
+#pragma unroll
+    for (int j = 0; j < kRowsPerWarp; ++j) {
+      const int i = warp + j * (THREADS / 32);
+      if (i < TR + 2) {
+        const int gr = min(max(r0 - 1 + i, 0), rows - 1);
+        const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr) * cols;
+        q[j] = __ldg(reinterpret_cast<const uint4*>(grow + c0) + lane);
+        if (lane < 2) halo[j] = __ldg(grow + (lane == 0 ? max(c0 - 1, 0) : min(c0 + TC, cols - 1)));
+      }
     }
-    if (lane == 0) srow[kPad - 1] = grow[max(c0 - 1, 0)];
-    if (lane == 1) srow[kPad + TC] = grow[min(c0 + TC, cols - 1)];
+#pragma unroll
+    for (int j = 0; j < kRowsPerWarp; ++j) {
+      const int i = warp + j * (THREADS / 32);
+      if (i < TR + 2) {
+        reinterpret_cast<uint4*>(tile[i] + kPad)[lane] = q[j];
+        if (lane < 2) tile[i][lane == 0 ? kPad - 1 : kPad + TC] = static_cast<std::uint16_t>(halo[j]);
+      }
+    }
+  } else {
+    for (int i = warp; i < TR + 2; i += THREADS / 32) {
+      const int gr = min(max(r0 - 1 + i, 0), rows - 1);
+      const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr) * cols;
+      std::uint16_t* srow = tile[i];
+      for (int c = lane; c < TC; c += 32) srow[kPad + c] = grow[min(c0 + c, cols - 1)];
+      if (lane == 0) srow[kPad - 1] = grow[max(c0 - 1, 0)];
+      if (lane == 1) srow[kPad + TC] = grow[min(c0 + TC, cols - 1)];
+    }
   }
   __syncthreads();
 
@@ -94,55 +170,29 @@ __global__ void __launch_bounds__(THREADS, 4)
   const int x0 = kPad + 8 * tx;
   const int col0 = c0 + 8 * tx;
   if (col0 >= cols) return;
-  // rows 2ty-1 .. 2ty+2 of the tile (smem rows 2ty .. 2ty+3)
-  const Row10 rw[4] = {load_row(tile[2 * ty], x0), load_row(tile[2 * ty + 1], x0),
-                       load_row(tile[2 * ty + 2], x0), load_row(tile[2 * ty + 3], x0)};
+  // image rows RPT*ty-1 .. RPT*ty+RPT of the tile (smem rows RPT*ty ..
+  // RPT*ty+RPT+1); each further row is read after the previous output row
+  // is stored (fewer live registers).
+  Row10 rw[RPT + 2];
+  rw[0] = load_row(tile[RPT * ty], x0);
+  rw[1] = load_row(tile[RPT * ty + 1], x0);
+  rw[2] = load_row(tile[RPT * ty + 2], x0);
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int row = r0 + 2 * ty + rr;
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int row = r0 + RPT * ty + rr;
     if (row >= rows) break;
-    const Row10& up = rw[rr];
-    const Row10& mid = rw[rr + 1];
-    const Row10& dn = rw[rr + 2];
-    const bool even_row = ((row + dr) & 1) == 0;
+    if (rr >= 1) rw[rr + 2] = load_row(tile[RPT * ty + rr + 2], x0);
     std::uint32_t pr[8], pg[8], pb[8];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) {
-      const bool even_col = ((col0 + cc + dc) & 1) == 0;
-      const std::uint32_t s = mid.v[cc + 1];
-      const std::uint32_t n = up.v[cc + 1], so = dn.v[cc + 1];
-      const std::uint32_t w = mid.v[cc], e = mid.v[cc + 2];
-      if (even_row == even_col) {  // R (even/even) or B (odd/odd) site
-        std::uint32_t g;
-        if constexpr (kGradient) {
-          const std::uint32_t dh = w > e ? w - e : e - w;
-          const std::uint32_t dv = n > so ? n - so : so - n;
-          g = dh < dv ? avg2(w, e) : (dv < dh ? avg2(n, so) : avg4(n, so, w, e));
-        } else {
-          g = avg4(n, so, w, e);
-        }
-        const std::uint32_t diag = avg4(up.v[cc], up.v[cc + 2], dn.v[cc], dn.v[cc + 2]);
-        pg[cc] = g;
-        pr[cc] = even_row ? s : diag;
-        pb[cc] = even_row ? diag : s;
-      } else {
-        pg[cc] = s;
-        const std::uint32_t ew = avg2(w, e), ns = avg2(n, so);
-        pr[cc] = even_row ? ew : ns;  // G in a red row: R from E/W
-        pb[cc] = even_row ? ns : ew;
-      }
-    }
+    // row parity is warp-uniform (a warp owns one row pair)
+    if (((row + dr) & 1) == 0)
+      mosaic_row<kGradient, true, kDc>(rw[rr], rw[rr + 1], rw[rr + 2], pr, pg, pb);
+    else
+      mosaic_row<kGradient, false, kDc>(rw[rr], rw[rr + 1], rw[rr + 2], pr, pg, pb);
     const std::uint64_t off = static_cast<std::uint64_t>(row) * cols + col0;
     if (vec_ok && col0 + 8 <= cols) {
-      const uint4 vr = make_uint4(pr[0] | (pr[1] << 16), pr[2] | (pr[3] << 16), pr[4] | (pr[5] << 16),
-                                  pr[6] | (pr[7] << 16));
-      const uint4 vg = make_uint4(pg[0] | (pg[1] << 16), pg[2] | (pg[3] << 16), pg[4] | (pg[5] << 16),
-                                  pg[6] | (pg[7] << 16));
-      const uint4 vb = make_uint4(pb[0] | (pb[1] << 16), pb[2] | (pb[3] << 16), pb[4] | (pb[5] << 16),
-                                  pb[6] | (pb[7] << 16));
-      __stcs(reinterpret_cast<uint4*>(out + off), vr);
-      __stcs(reinterpret_cast<uint4*>(out + plane + off), vg);
-      __stcs(reinterpret_cast<uint4*>(out + 2 * plane + off), vb);
+      __stcs(reinterpret_cast<uint4*>(out + off), pack8(pr));
+      __stcs(reinterpret_cast<uint4*>(out + plane + off), pack8(pg));
+      __stcs(reinterpret_cast<uint4*>(out + 2 * plane + off), pack8(pb));
     } else {
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
@@ -170,12 +220,23 @@ void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* ou
   // 128-bit paths need every row and every plane to start 16-byte aligned.
   const int vec_ok = (cols % 8 == 0) && (plane % 8 == 0) &&
                      (((reinterpret_cast<std::uintptr_t>(out) | reinterpret_cast<std::uintptr_t>(in)) & 15) == 0);
-  const dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + TR - 1) / TR));
+  // The column phase selects the kernel (site types are compile-time per
+  // column).  Rows per thread: 4 for bilinear, 8 for gradient (16384^2 on a
+  // B200: bilinear 0.340 / 0.346 ms, gradient 0.383 / 0.368 ms at 4 / 8);
+  // GPCX_DEMOSAIC_RPT=4|8 overrides for A/B runs.
+  static const int rpt_env = [] {
+    const char* v = std::getenv("GPCX_DEMOSAIC_RPT");
+    return v == nullptr ? 0 : (v[0] == '8' ? 8 : 4);
+  }();
+  const int rpt = rpt_env != 0 ? rpt_env : (gradient ? 8 : 4);
+  const std::uint64_t tr = 8u * rpt;
+  const dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + tr - 1) / tr));
   if (grid.y > 65535) fail(Errc::TooLarge, "too many rows for the tile grid");
-  if (gradient)
-    demosaic_kernel<true><<<grid, THREADS, 0, stream>>>(in, out, (int)rows, (int)cols, dr, dc, vec_ok);
-  else
-    demosaic_kernel<false><<<grid, THREADS, 0, stream>>>(in, out, (int)rows, (int)cols, dr, dc, vec_ok);
+  auto kernel = rpt == 8 ? (gradient ? (dc ? demosaic_kernel<true, 1, 8> : demosaic_kernel<true, 0, 8>)
+                                     : (dc ? demosaic_kernel<false, 1, 8> : demosaic_kernel<false, 0, 8>))
+                         : (gradient ? (dc ? demosaic_kernel<true, 1, 4> : demosaic_kernel<true, 0, 4>)
+                                     : (dc ? demosaic_kernel<false, 1, 4> : demosaic_kernel<false, 0, 4>));
+  kernel<<<grid, THREADS, 0, stream>>>(in, out, (int)rows, (int)cols, dr, vec_ok);
   GPCX_LAUNCH_CHECK();
 }
 
