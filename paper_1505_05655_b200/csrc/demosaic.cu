@@ -89,9 +89,13 @@ __device__ __forceinline__ void mosaic_row(const Row10& up, const Row10& mid, co
     if (kEvenRow == even_col) {  // R (even/even) or B (odd/odd) site
       std::uint32_t g;
       if constexpr (kGradient) {
+        // avg2(x, y) = (2(x + y) + 2) >> 2, so the three candidates share
+        // one shift: pick the numerator, then g = t >> 2.
         const std::uint32_t dh = w > e ? w - e : e - w;
         const std::uint32_t dv = n > so ? n - so : so - n;
-        g = dh < dv ? avg2(w, e) : (dv < dh ? avg2(n, so) : avg4(n, so, w, e));
+        const std::uint32_t sh = w + e, sv = n + so;
+        const std::uint32_t t = dh < dv ? 2 * sh : (dv < dh ? 2 * sv : sh + sv);
+        g = (t + 2) >> 2;
       } else {
         g = avg4(n, so, w, e);
       }
