@@ -175,3 +175,40 @@ def test_devinfo_reports_the_b200(gpu):
     assert xml.startswith('<?xml version="1.0"?>\n<gpgpu_server>\n  <device index="0">\n')
     assert "<multi_processor_count>148</multi_processor_count>" in xml
     assert G.parse_params(resp["params"])["devices"] == str(len(devs))
+
+
+_RPT_CHECK = r"""
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import test_demosaic as T
+from oracle import oracle as O
+bad = []
+for gradient in (False, True):
+    for rows, cols in [(31, 264), (32, 256), (33, 257), (63, 520), (64, 512), (65, 130),
+                       (127, 776), (129, 2056), (200, 8)]:
+        rng = np.random.default_rng(rows * 7 + cols)
+        for phase in T.PHASES:
+            img = T._mosaic(rng, rows, cols)
+            if not np.array_equal(T._gpu_demosaic(gradient, phase, img, rows, cols),
+                                  O.ref_demosaic(gradient, img, rows, cols, phase)):
+                bad.append((gradient, rows, cols, phase))
+print("BAD", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rpt", ["4", "8"])
+def test_both_tile_heights_equal_reference(gpu, refl, rpt):
+    """The launcher picks 4 rows per thread (32-row tiles) for bilinear and 8
+    (64-row tiles) for gradient; GPCX_DEMOSAIC_RPT forces one height for
+    both.  Each height, both kernels, all phases, tile-edge sizes."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, GPCX_DEMOSAIC_RPT=rpt)
+    r = subprocess.run([sys.executable, "-c", _RPT_CHECK], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
