@@ -196,6 +196,47 @@ def band(rows: int, n: int, r: int) -> tuple[int, int]:
 
 # ------------------------------------------------------------- B200 legs ---
 
+def exchange_mode(d: Dist) -> str:
+    """N>1 histogram exchange: "peer" (fused into the kernel over NVLink peer
+    memory, gpcx_lut_peer_*) unless GPCX_LUT_EXCHANGE=nccl; the single-GPU
+    test mode defaults to the NCCL/gloo path (its ranks share one GPU and
+    would meet only through time-slicing)."""
+    want = os.environ.get("GPCX_LUT_EXCHANGE", "")
+    if want in ("peer", "nccl"):
+        return want
+    return "nccl" if Dist.one_gpu else "peer"
+
+
+def open_peer_exchange(d: Dist, make_peer, dev):
+    """Create this rank's exchange block, all-gather the IPC handles and
+    connect -- or, if ANY rank fails (no P2P path, allocation failure),
+    return None on every rank so all of them use the NCCL exchange."""
+    import torch
+    peer = mine = None
+    try:
+        peer = make_peer()
+        mine = peer.handle()
+    except Exception as e:
+        print(f"rank {d.rank}: peer exchange unavailable ({e}); using NCCL", file=sys.stderr)
+    handles = [None] * d.n
+    d.pg.all_gather_object(handles, mine)  # every rank takes part, even after a failure
+    ok = int(all(h is not None for h in handles))
+    if ok:
+        try:
+            peer.connect(handles)
+        except Exception as e:
+            print(f"rank {d.rank}: peer exchange unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32,
+                        device=dev if d.pg.get_backend() == "nccl" else "cpu")
+    d.pg.all_reduce(flag, op=d.pg.ReduceOp.MIN)
+    if int(flag.item()) == 0:
+        if peer is not None:
+            peer.close()
+        return None
+    return peer
+
+
 def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     import torch
     from paper_1505_05655_b200 import device as D
@@ -210,12 +251,22 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     stream = torch.cuda.current_stream()
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     ev = {k: [] for k in ("h0", "h1", "a0", "a1")}
+    peer = None
+    if d.pg is not None and exchange_mode(d) == "peer":
+        # histogram exchange fused into the kernel over peer memory: IPC
+        # handles of every rank's exchange block, all-gathered once
+        peer = open_peer_exchange(d, lambda: D.LutPeer(d.rank, d.n), dev)
 
     def step(record: bool):
         if record:
             ev["h0"].append(E()); ev["h0"][-1].record(stream)
         if d.pg is None:  # one GPU: ONE cooperative launch (histogram -> LUT -> apply)
             D.lut_correct(img, out, mode, lut, stats, ws, stream)
+            if record:
+                ev["h1"].append(E()); ev["h1"][-1].record(stream)
+            return
+        if peer is not None:  # N GPUs, still ONE launch per rank per step
+            peer.correct(img, out, mode, lut, stats, ws, stream)
             if record:
                 ev["h1"].append(E()); ev["h1"][-1].record(stream)
             return
@@ -255,8 +306,13 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
     st = D.read_stats(stats)
     gather_ms = gather_leg(d, out) if d.pg is not None else None
+    if peer is not None:
+        d.barrier()  # no rank unmaps its exchange block while a peer may still read it
+        torch.cuda.synchronize()
+        peer.close()
     return {"ms": ms, "hist_ms": hist_ms, "exch_ms": exch_ms, "band_px": n, "digest": dig,
-            "stats": st, "clocks": clk.summary(), "gather_ms": gather_ms}
+            "stats": st, "clocks": clk.summary(), "gather_ms": gather_ms,
+            "exchange": None if d.pg is None else ("peer" if peer is not None else "nccl")}
 
 
 def gather_leg(d: Dist, out, reps: int = 3) -> float:
@@ -734,8 +790,9 @@ def run_b200(args) -> None:
     band_px = lut["band_px"]
     tr = traffic_from_profiles()
     step_ach = 6.0 * band_px / (ms / args.steps / 1e3) / 1e9
-    # fused_kernel launches (1 at N=1; count, then build+apply around the
-    # NCCL all-reduce at N>1) carry the step's 6 B/px of algorithmic traffic.
+    # fused_kernel launches (1 at N=1 and with the peer exchange at N>1;
+    # count, then build+apply around the NCCL all-reduce otherwise) carry
+    # the step's 6 B/px of algorithmic traffic.
     kern_ms = hist_ms - (exch_ms or 0.0)
     fused_ach = 6.0 * band_px / (kern_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "kernel": "lut::fused_kernel", "achieved": round(fused_ach, 1),
@@ -750,6 +807,10 @@ def run_b200(args) -> None:
                                  "algorithmic_bytes": 6 * band_px}}}
     if exch_ms is not None:
         roof["kernels"]["histogram_all_reduce"] = {"ms": round(exch_ms, 4), "bytes": 262144}
+    if lut["exchange"] == "peer":
+        roof["kernels"]["fused_kernel"]["phases"] = (
+            "histogram (2 B/px) | publish slice + system-scope flag rendezvous + P2P sum of the "
+            "peers' slices | LUT | apply (4 B/px)")
     gather = None
     if gather_ms is not None:
         gather = {"ms": round(gather_ms, 3), "bytes": 2 * ROWS * COLS,
@@ -763,9 +824,13 @@ def run_b200(args) -> None:
             "data": "synthetic (ramp12 splitmix64 scene, generated on device)",
             "config": {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene, row bands",
                        "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
-                       "parallelism": f"row-band x{d.n}, NCCL all-reduce of the 65536-bin histogram",
+                       "parallelism": (f"row-band x{d.n}" if d.n == 1 else
+                                       f"row-band x{d.n}, 65536-bin histogram exchange: "
+                                       + ("fused into the kernel over peer memory (IPC / NVLink P2P)"
+                                          if lut["exchange"] == "peer" else "NCCL all-reduce")),
                        "l2": "inputs larger than L2 (2 GiB scene)"},
-            # per step: fused_kernel once at N=1; count + build/apply launches at N>1
+            # per step: fused_kernel once (N=1, or N>1 with the peer exchange);
+            # count + build/apply launches with the NCCL exchange
             "roofline": roof, "gpu_launches": launches * args.steps,
             "clocks": lut["clocks"]}
     if gather is not None:

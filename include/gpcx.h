@@ -207,6 +207,31 @@ int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n,
                             int mode, uint16_t* lut, gpcx_lut_stats* stats,
                             void* ws, uint64_t ws_bytes, void* stream);
 
+/* Row-band sharded LUT_CORRECT / LUT_GEN with one process per GPU and the
+ * histogram exchange fused into the kernel over peer memory (no NCCL; the
+ * reference has no multi-GPU path -- SURVEY.md §8e's "one exchange step").
+ *   1. every rank: gpcx_lut_peer_create(rank, nranks, &p) on its device and
+ *      gpcx_lut_peer_ipc_handle(p, h) (GPCX_IPC_HANDLE_BYTES bytes);
+ *   2. the handles are all-gathered by the caller (torch.distributed, MPI,
+ *      a file ...) in rank order and passed to gpcx_lut_peer_connect;
+ *   3. every rank issues the SAME sequence of gpcx_lut_correct_peer_device
+ *      calls on its band (out == NULL: LUT + stats only).  Each call is one
+ *      cooperative launch: count the band, publish it, meet the peers
+ *      (system-scope flags), sum their histograms with P2P loads, build the
+ *      identical LUT on every rank, apply it to the band.
+ * A rank whose peers never arrive traps after GPCX_PEER_TIMEOUT_MS (default
+ * 60000) and the call's stream reports the failure. */
+#define GPCX_IPC_HANDLE_BYTES 64
+typedef struct gpcx_lut_peer gpcx_lut_peer;
+int gpcx_lut_peer_create(int rank, int nranks, gpcx_lut_peer** out);
+int gpcx_lut_peer_ipc_handle(const gpcx_lut_peer* p, void* handle);
+int gpcx_lut_peer_connect(gpcx_lut_peer* p, const void* handles);
+int gpcx_lut_peer_destroy(gpcx_lut_peer* p);
+int gpcx_lut_correct_peer_device(gpcx_lut_peer* p, const uint16_t* in, uint16_t* out,
+                                 uint64_t n, int mode, uint16_t* lut,
+                                 gpcx_lut_stats* stats, void* ws, uint64_t ws_bytes,
+                                 void* stream);
+
 /* C (m x n) = A (m x k) * B (k x n), all f32 row-major with leading
  * dimensions lda/ldb/ldc (elements).  prec selects the path (GPCX_PREC_*). */
 int gpcx_matmul_workspace_size(int prec, uint64_t m, uint64_t n, uint64_t k,

@@ -42,7 +42,10 @@ EXPORTS = [
     "gpcx_matmul_device", "gpcx_synth_image_device", "gpcx_synth_matrix_device",
     "gpcx_digest_u16_device", "gpcx_server_start", "gpcx_server_stop", "gpcx_handle_request",
     "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render", "gpcx_client_submit",
+    "gpcx_lut_peer_create", "gpcx_lut_peer_ipc_handle", "gpcx_lut_peer_connect",
+    "gpcx_lut_peer_destroy", "gpcx_lut_correct_peer_device",
 ]
+IPC_HANDLE_BYTES = 64
 
 PHASES = {"RGGB": 0, "BGGR": 1, "GRBG": 2, "GBRG": 3}
 
@@ -116,6 +119,11 @@ def _load() -> C.CDLL:
         "gpcx_devinfo_render": ([vp, i32, cp, u64, pu64], i32),
         "gpcx_client_submit": ([cp, C.c_uint16, cp, cp, C.POINTER(vp), pu64, i32, cp, vp, u64, pu64,
                                 cp, u64, cp, u64], i32),
+        "gpcx_lut_peer_create": ([i32, i32, C.POINTER(vp)], i32),
+        "gpcx_lut_peer_ipc_handle": ([vp, vp], i32),
+        "gpcx_lut_peer_connect": ([vp, vp], i32),
+        "gpcx_lut_peer_destroy": ([vp], i32),
+        "gpcx_lut_correct_peer_device": ([vp, vp, vp, u64, i32, vp, vp, vp, u64, vp], i32),
     }
     assert set(sig) == set(EXPORTS)
     for name, (args, res) in sig.items():

@@ -35,6 +35,7 @@ CPP_SOURCES = [
     "host/task_spec.cpp",
     "host/runtime.cpp",
     "host/executor.cpp",
+    "host/peer.cpp",
     "host/devinfo.cpp",
     "host/registry.cpp",
     "host/net.cpp",

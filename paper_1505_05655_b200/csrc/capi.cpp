@@ -5,12 +5,14 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/gpcx.h"
 #include "cuda_util.hpp"
 #include "host/devinfo.hpp"
 #include "host/executor.hpp"
 #include "host/net.hpp"
+#include "host/peer.hpp"
 #include "host/registry.hpp"
 #include "host/runtime.hpp"
 #include "host/server.hpp"
@@ -303,6 +305,54 @@ int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n, int m
     if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
       gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
     gpcx::lut::launch_correct(in, out, n, mode, lut, stats, ws, as_stream(stream));
+  });
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == GPCX_IPC_HANDLE_BYTES, "IPC handle size");
+
+struct gpcx_lut_peer {
+  gpcx::peer::LutRank rank;
+  gpcx_lut_peer(int r, int n) : rank(r, n) {}
+};
+
+int gpcx_lut_peer_create(int rank, int nranks, gpcx_lut_peer** out) {
+  return guarded([&] {
+    if (out == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null output");
+    *out = new gpcx_lut_peer(rank, nranks);
+  });
+}
+
+int gpcx_lut_peer_ipc_handle(const gpcx_lut_peer* p, void* handle) {
+  return guarded([&] {
+    if (p == nullptr || handle == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null argument");
+    const cudaIpcMemHandle_t h = p->rank.handle();
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int gpcx_lut_peer_connect(gpcx_lut_peer* p, const void* handles) {
+  return guarded([&] {
+    if (p == nullptr || handles == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null argument");
+    std::vector<cudaIpcMemHandle_t> hs(p->rank.nranks());
+    std::memcpy(hs.data(), handles, hs.size() * sizeof(cudaIpcMemHandle_t));
+    p->rank.connect(hs.data());
+  });
+}
+
+int gpcx_lut_peer_destroy(gpcx_lut_peer* p) {
+  return guarded([&] { delete p; });
+}
+
+int gpcx_lut_correct_peer_device(gpcx_lut_peer* p, const uint16_t* in, uint16_t* out,
+                                 uint64_t n, int mode, uint16_t* lut, gpcx_lut_stats* stats,
+                                 void* ws, uint64_t ws_bytes, void* stream) {
+  return guarded([&] {
+    if (p == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null peer group");
+    if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
+      gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
+    need_u32(n);
+    need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
+    p->rank.correct(in, out, n, mode, lut, stats, ws, as_stream(stream));
   });
 }
 

@@ -115,6 +115,22 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
   const bool need_apply = flag != Flag::LutGen;
   const bool equalize = p.mode == GPCX_LUT_EQUALIZE;
 
+  // Equalize exchange over peer memory when every band's device can load
+  // every other band's histogram (NVLink P2P, or the same device).
+  bool peer_sum = G > 1 && G <= static_cast<std::size_t>(lut::kMaxRanks);
+  for (std::size_t i = 0; peer_sum && i < G; ++i)
+    for (std::size_t j = 0; peer_sum && j < G; ++j)
+      peer_sum = rt::peer_reachable(leases[i]->device, leases[j]->device);
+  std::vector<lut::PeerTable> tables(G);
+  if (peer_sum) {
+    for (std::size_t i = 0; i < G; ++i) {
+      tables[i].rank = static_cast<int>(i);
+      tables[i].nranks = static_cast<int>(G);
+      for (std::size_t r = 0; r < G; ++r)
+        tables[i].hist[0][r] = tables[i].hist[1][r] = leases[r]->d_hist();
+    }
+  }
+
   // Phase 1: stage each band into HBM; local statistics.
   std::vector<std::vector<std::uint32_t>> hists(G);
   std::vector<gpcx_lut_stats> local(G);
@@ -130,7 +146,13 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       return;
     }
     if (G == 1) return;  // single device: generate in phase 2 directly
-    if (equalize) {
+    if (equalize && peer_sum) {
+      // the band histogram stays in HBM; phase 2 sums the bands' histograms
+      // with P2P loads (lut::launch_correct_from_peers) after every band's
+      // `ready` event -- no device -> host -> device round trip
+      lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream);
+      GPCX_CUDA(cudaEventRecord(s.ready, s.stream));
+    } else if (equalize) {
       lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream);
       hists[i].resize(65536);
       rt::d2h(s, hists[i].data(), s.d_hist(), 65536 * 4);
@@ -145,7 +167,9 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
   std::vector<std::uint32_t> global_hist;
   gpcx_lut_stats global_mm{n, 0xFFFFFFFFu, 0, 0};
   if (G > 1 && flag != Flag::LutApply) {
-    if (equalize) {
+    if (equalize && peer_sum) {
+      // summed on the devices in phase 2
+    } else if (equalize) {
       global_hist.assign(65536, 0);
       for (const auto& h : hists)
         for (int v = 0; v < 65536; ++v) global_hist[v] += h[v];
@@ -176,6 +200,14 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
           lut::launch_minmax(dimg, bn, s.d_stats(), s.lut_ws.ptr, s.stream);
           lut::launch_from_minmax(s.d_stats(), s.d_lut(), s.stream);
         }
+      } else if (equalize && peer_sum) {
+        for (std::size_t r = 0; r < G; ++r)
+          if (r != i) GPCX_CUDA(cudaStreamWaitEvent(s.stream, leases[r]->ready, 0));
+        GPCX_CUDA(cudaMemcpyAsync(s.d_peer_table(), &tables[i], sizeof(lut::PeerTable),
+                                  cudaMemcpyHostToDevice, s.stream));
+        lut::launch_correct_from_peers(s.d_peer_table(), 0, p.mode, dimg,
+                                       need_apply ? dimg : nullptr, bn, s.d_lut(), s.d_stats(),
+                                       s.lut_ws.ptr, s.stream);
       } else if (equalize) {
         GPCX_CUDA(cudaMemcpyAsync(s.d_hist(), global_hist.data(), 65536 * 4,
                                   cudaMemcpyHostToDevice, s.stream));

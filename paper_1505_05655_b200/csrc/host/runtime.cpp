@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../cuda_util.hpp"
 #include "../kernels.hpp"
@@ -71,21 +74,33 @@ namespace {
 // Direct NVLink access between every pair of bound devices, so a peer copy
 // (cudaMemcpyPeerAsync) is one DMA over NVSwitch instead of a host bounce.
 // Best effort: without it the copies still work, just staged.
+std::mutex g_peer_mu;
+std::set<std::pair<int, int>> g_peer_on;  // (d, p): d may load p's memory
+
 void enable_peer_access(const std::vector<int>& devs) {
   int cur = 0;
   if (cudaGetDevice(&cur) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lock(g_peer_mu);
   for (int d : devs) {
     for (int p : devs) {
       if (p == d) continue;
       int can = 0;
       if (cudaDeviceCanAccessPeer(&can, d, p) != cudaSuccess || !can) continue;
       cudaSetDevice(d);
-      if (cudaDeviceEnablePeerAccess(p, 0) != cudaSuccess) cudaGetLastError();
+      const cudaError_t e = cudaDeviceEnablePeerAccess(p, 0);
+      if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) g_peer_on.insert({d, p});
+      if (e != cudaSuccess) cudaGetLastError();
     }
   }
   cudaSetDevice(cur);
 }
 }  // namespace
+
+bool peer_reachable(int from, int to) {
+  if (from == to) return true;
+  std::lock_guard<std::mutex> lock(g_peer_mu);
+  return g_peer_on.count({from, to}) != 0;
+}
 
 void Runtime::init(const std::vector<int>& devices) {
   std::lock_guard<std::mutex> lock(mu_);
@@ -167,7 +182,7 @@ SlotLease Runtime::acquire(int device_index) {
   for (cudaEvent_t& e : slot->chunk_done)
     GPCX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   GPCX_CUDA(cudaEventCreateWithFlags(&slot->ready, cudaEventDisableTiming));
-  slot->small.ensure(131072 + 256 + 65536 * 4);
+  slot->small.ensure(131072 + 256 + 65536 * 4 + sizeof(lut::PeerTable));
   slot->h_small.ensure(256);
   slot->lut_ws.ensure(lut::workspace_bytes(), /*zero=*/true);
   Slot* raw = slot.get();

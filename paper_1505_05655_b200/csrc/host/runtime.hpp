@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../../include/gpcx.h"
+#include "../kernels.hpp"
 
 namespace gpcx::rt {
 
@@ -61,6 +62,11 @@ struct Slot {
   }
   std::uint32_t* d_hist() const {
     return reinterpret_cast<std::uint32_t*>(small.as<unsigned char>() + 131072 + 256);
+  }
+  // device copy of the band's PeerTable (the in-process LUT exchange)
+  lut::PeerTable* d_peer_table() const {
+    return reinterpret_cast<lut::PeerTable*>(small.as<unsigned char>() + 131072 + 256 +
+                                             65536 * 4);
   }
   gpcx_lut_stats* h_stats() const { return static_cast<gpcx_lut_stats*>(h_small.ptr); }
   ~Slot();
@@ -173,5 +179,7 @@ void pinned_trim();  // frees idle pooled buffers
 
 // Makes `device` current for the calling thread.
 void use_device(int device);
+// true when `from` has peer access to `to`'s memory (or from == to).
+bool peer_reachable(int from, int to);
 
 }  // namespace gpcx::rt

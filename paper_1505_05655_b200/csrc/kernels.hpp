@@ -30,6 +30,47 @@ std::uint32_t* ws_hist(void* ws);
 
 int parts_for(std::uint64_t n, int num_sms);
 
+// ---- multi-GPU histogram exchange over peer memory (no NCCL) ----------
+// Rank r of a group publishes its band histogram in its own HBM; the fused
+// kernel of every rank sums the group's histograms slice by slice with
+// system-scope loads of the peers' buffers (NVLink P2P / CUDA IPC
+// mappings).  Two ways to order it:
+//   flags != nullptr  device-side: after writing slice b, rank r's slice
+//                     CTA b stores seq into flags[q][b][r] of every rank q
+//                     (release, system scope) and waits until its own
+//                     flags[r][b][*] >= seq (acquire) -- one launch per step
+//                     and no host round trip (one process per GPU);
+//   flags == nullptr  host-ordered: the caller guarantees every rank's
+//                     histogram is complete before the launch (the
+//                     in-process planner joins its band threads).
+// Histogram buffers are double-buffered by seq parity, so a rank that runs
+// ahead into step seq+1 never overwrites what a slower peer still reads.
+inline constexpr int kMaxRanks = 8;
+inline constexpr int kFlagSlices = 128;  // one flag row per phase-2 slice CTA
+struct PeerTable {
+  int rank = 0, nranks = 1;
+  std::uint32_t* flags[kMaxRanks] = {};    // rank q's flag block: [kFlagSlices][kMaxRanks] u32
+  std::uint32_t* hist[2][kMaxRanks] = {};  // rank q's histogram (u32[65536]) by seq parity
+};
+// One rank's device block: hist[2][65536] u32 | flags | its PeerTable.
+inline constexpr std::uint64_t kPeerHistBytes = 2ull * kBins * 4;
+inline constexpr std::uint64_t kPeerFlagBytes = std::uint64_t(kFlagSlices) * kMaxRanks * 4;
+inline constexpr std::uint64_t kPeerBlockBytes = kPeerHistBytes + kPeerFlagBytes + 4096;
+// LUT_CORRECT / LUT_GEN of one rank's band with the exchange fused into the
+// cooperative kernel: stages count (+ publish) -> exchange -> LUT -> apply
+// (out == nullptr: LUT only).  `table` is the device copy of the rank's
+// PeerTable, `own_hist` = its hist[seq & 1][rank].
+void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::uint32_t seq,
+                         std::uint64_t timeout_ns, const std::uint16_t* in, std::uint16_t* out,
+                         std::uint64_t n, int mode, std::uint16_t* lut, gpcx_lut_stats* stats,
+                         void* ws, cudaStream_t stream);
+// Host-ordered second half for the in-process planner: sum the group's
+// published histograms (table->flags unused), LUT, apply the band.
+void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mode,
+                               const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
+                               std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
+                               cudaStream_t stream);
+
 // Histogram of img into hist (u32[65536]).
 void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
                  void* ws, cudaStream_t stream);

@@ -275,20 +275,71 @@ __device__ unsigned long long* g_lut_trace;
 //   kApply   grid.sync; phase 4  every CTA stages the LUT in smem (over the dead
 //                     bins) and maps the image -- which, at C1 size, phase 1
 //                     left in L2.
+//   kExchange (N devices)  in phase 2, after a slice CTA has merged its 512
+//            bins of this rank's band histogram (published in the rank's
+//            HBM), it meets the same slice CTA of every other rank (system-
+//            scope release/acquire flags, peer_rendezvous) and sums their
+//            slices with P2P loads -- the histogram all-reduce, fused, one
+//            slice at a time, so no grid-wide or host synchronisation.
 // Single device LUT_CORRECT = kCount|kBuild|kApply, LUT_GEN = kCount|kBuild;
-// N devices: kCount -> all-reduce(hist) -> kBuild|kApply.  No launch gaps,
-// and the partial merge is not latency-bound like a one-thread-per-bin sum.
-enum Stage : int { kCount = 1, kBuild = 2, kApply = 4 };
+// N devices, one process per GPU: kCount|kExchange|kBuild|kApply (one
+// launch per rank); in-process planner: kCount, then kExchange|kBuild|kApply
+// after the bands' events (host-ordered, no flags); NCCL fallback:
+// kCount -> all-reduce(hist) -> kBuild|kApply.  No launch gaps, and the
+// partial merge is not latency-bound like a one-thread-per-bin sum.
+enum Stage : int { kCount = 1, kBuild = 2, kApply = 4, kExchange = 8 };
 constexpr int kSlices = kWords / 256;    // 128 CTAs own 512 bins in phases 2-3
 constexpr int kGroups = kThreads / 64;   // partial groups per slice
 static_assert(kGroups * 512 * 4 <= kWords * 4, "phase-2 reduction fits in the bins");
+static_assert(kSlices == kFlagSlices, "one flag row per slice CTA");
+
+__device__ __forceinline__ void st_release_sys(std::uint32_t* p, std::uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_relaxed_sys(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.relaxed.sys.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device-side rendezvous of slice `slice` across the group (thread 0 of the
+// slice CTA, after the CTA's words of the slice are in this rank's
+// published histogram): publish seq to every rank's flag row, then wait
+// for every rank's seq in our own row.  A peer that never arrives (dead
+// process, mismatched seq) traps after timeout_ns instead of hanging the GPU.
+__device__ void peer_rendezvous(const PeerTable* P, int slice, std::uint32_t seq,
+                                unsigned long long timeout_ns) {
+  const int me = P->rank, nr = P->nranks;
+  __threadfence_system();
+  for (int r = 0; r < nr; ++r) st_release_sys(P->flags[r] + slice * kMaxRanks + me, seq);
+  const std::uint32_t* row = P->flags[me] + slice * kMaxRanks;
+  const unsigned long long t0 = globaltimer_ns();
+  for (int r = 0; r < nr; ++r) {
+    // >= (wrap-aware): a peer may already be publishing seq + 1
+    while (static_cast<int>(ld_acquire_sys(row + r) - seq) < 0) {
+      __nanosleep(100);
+      if (globaltimer_ns() - t0 > timeout_ns) __trap();
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int nparts,
                  uint32_t* __restrict__ parts, uint32_t* __restrict__ overflow,
                  uint32_t* __restrict__ hist, uint4* __restrict__ blocks, int mode,
                  std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
-                 int stages) {
+                 int stages, const PeerTable* __restrict__ peers, std::uint32_t seq,
+                 unsigned long long timeout_ns) {
   extern __shared__ uint4 smem_u4[];
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
   __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8], s_wfcount[8];
@@ -341,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
     }
     __syncthreads();
+    const bool exchange = stages & kExchange;
     if (t < 256) {
       if (count) {
         uint32_t lo = 0, hi = 0;
@@ -354,11 +406,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         c0 = lo + ov.x;
         c1 = hi + ov.y;
         reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
-      } else {
+      } else if (!exchange) {
         const uint2 h = __ldcg(reinterpret_cast<const uint2*>(hist) + w);
         c0 = h.x;
         c1 = h.y;
       }
+    }
+    if (exchange) {
+      // multi-GPU: this slice of every rank's band histogram, summed with
+      // system-scope loads of the peers' HBM (the all-reduce, fused)
+      const int par = seq & 1;
+      if (peers->flags[0] != nullptr) {
+        __syncthreads();  // this CTA's words of the slice are published
+        if (t == 0) peer_rendezvous(peers, blockIdx.x, seq, timeout_ns);
+        __syncthreads();
+      }
+      if (t < 256) {
+        const int me = count ? peers->rank : -1;  // own counts are in c0 / c1
+        for (int r = 0; r < peers->nranks; ++r) {
+          if (r == me) continue;
+          const uint2 h = ld_relaxed_sys(reinterpret_cast<const uint2*>(peers->hist[par][r]) + w);
+          c0 += h.x;
+          c1 += h.y;
+        }
+      }
+    }
+    if (t < 256) {
       inc = c0 + c1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -631,7 +704,8 @@ namespace {
 // fused_kernel over the whole device (see its comment for `stages`).
 void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std::uint64_t n,
                   uint32_t* hist, int mode, std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, const PeerTable* peers = nullptr, std::uint32_t seq = 0,
+                  unsigned long long timeout_ns = 0) {
   set_attrs_once();
   auto* base = static_cast<unsigned char*>(ws);
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
@@ -641,7 +715,8 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
   const int sms = device_sm_count();
   int nparts = parts_for(n, sms);
   void* args[] = {const_cast<std::uint16_t**>(&img), &out, &n, &nparts, &parts, &overflow,
-                  &hist, &blocks, &mode, &lut, &stats, &stages};
+                  &hist, &blocks, &mode, &lut, &stats, &stages,
+                  const_cast<PeerTable**>(&peers), &seq, &timeout_ns};
   GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fused_kernel),
                                         dim3(std::max(sms, kSlices)), dim3(kThreads), args,
                                         kSmemHist, stream));
@@ -692,6 +767,38 @@ void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n
     launch_minmax(in, n, stats, ws, stream);
     launch_from_minmax(stats, lut, stream);
   }
+  launch_apply(lut, in, out, n, stream);
+}
+
+void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::uint32_t seq,
+                         std::uint64_t timeout_ns, const std::uint16_t* in, std::uint16_t* out,
+                         std::uint64_t n, int mode, std::uint16_t* lut, gpcx_lut_stats* stats,
+                         void* ws, cudaStream_t stream) {
+  // every rank launches the same stages (the rendezvous sits in phase 2);
+  // the apply needs co-aligned in/out (the callers check) or out == nullptr
+  const bool fused_apply = out != nullptr && co_aligned(in, out);
+  const int stages = kCount | kExchange | kBuild | (fused_apply ? kApply : 0);
+  launch_fused(stages, in, fused_apply ? out : nullptr, n, own_hist, mode, lut, stats, ws,
+               stream, table, seq, timeout_ns);
+  if (out != nullptr && !fused_apply) launch_apply(lut, in, out, n, stream);
+}
+
+void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mode,
+                               const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
+                               std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
+                               cudaStream_t stream) {
+  if (out == nullptr || n == 0) {
+    launch_fused(kExchange | kBuild, nullptr, nullptr, 0, nullptr, mode, lut, stats, ws, stream,
+                 table, seq, 0);
+    return;
+  }
+  if (co_aligned(in, out)) {
+    launch_fused(kExchange | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream,
+                 table, seq, 0);
+    return;
+  }
+  launch_fused(kExchange | kBuild, nullptr, nullptr, 0, nullptr, mode, lut, stats, ws, stream,
+               table, seq, 0);
   launch_apply(lut, in, out, n, stream);
 }
 

@@ -11,7 +11,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import LutStats, check, lib
+from ._lib import IPC_HANDLE_BYTES, LutStats, check, lib
 
 STATS_BYTES = C.sizeof(LutStats)
 
@@ -80,6 +80,49 @@ def lut_apply(lut, inp, out, stream=None):
 def lut_correct(inp, out, mode, lut, stats, ws, stream=None):
     check(lib.gpcx_lut_correct_device(_p(inp), _p(out), inp.numel(), mode, _p(lut), _p(stats),
                                       _p(ws), ws.numel(), _s(stream)))
+
+
+class LutPeer:
+    """One rank of a row-band LUT group whose histogram exchange runs inside
+    the fused kernel over peer memory (gpcx_lut_peer_*, include/gpcx.h).
+
+        p = LutPeer(rank, nranks)            # on the rank's current device
+        handles = all_gather(p.handle())     # bytes, in rank order
+        p.connect(handles)
+        p.correct(band_in, band_out, mode, lut, stats, ws)   # every step
+    """
+
+    def __init__(self, rank: int, nranks: int):
+        self._p = C.c_void_p(None)
+        check(lib.gpcx_lut_peer_create(rank, nranks, C.byref(self._p)))
+        self.rank, self.nranks = rank, nranks
+
+    def handle(self) -> bytes:
+        buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+        check(lib.gpcx_lut_peer_ipc_handle(self._p, buf))
+        return bytes(buf)
+
+    def connect(self, handles) -> None:
+        blob = b"".join(handles)
+        assert len(blob) == IPC_HANDLE_BYTES * self.nranks
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(lib.gpcx_lut_peer_connect(self._p, buf))
+
+    def correct(self, inp, out, mode, lut, stats, ws, stream=None) -> None:
+        check(lib.gpcx_lut_correct_peer_device(self._p, _p(inp), None if out is None else _p(out),
+                                               inp.numel(), mode, _p(lut), _p(stats), _p(ws),
+                                               ws.numel(), _s(stream)))
+
+    def close(self) -> None:
+        if self._p:
+            check(lib.gpcx_lut_peer_destroy(self._p))
+            self._p = C.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def matmul_workspace(prec: int, m: int, n: int, k: int, device="cuda") -> torch.Tensor | None:

@@ -79,3 +79,51 @@ def test_sharded_lut_correct_over_gloo_equals_single_process(world, mode):
     assert out == r_out.tobytes()
     assert lut == r_lut.tobytes()
     assert stats == r_st
+
+
+class _FakePeer:
+    def __init__(self, rank, fail_at):
+        self.rank, self.fail_at, self.closed, self.connected = rank, fail_at, False, None
+        if fail_at == ("create", rank):
+            raise RuntimeError("no device block")
+
+    def handle(self):
+        return bytes([self.rank]) * 64
+
+    def connect(self, handles):
+        if self.fail_at == ("connect", self.rank):
+            raise RuntimeError("no P2P path")
+        self.connected = handles
+
+    def close(self):
+        self.closed = True
+
+
+def _negotiate_worker(rank, world, port, fail_at, q):
+    sys.path.insert(0, str(ROOT))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank))
+    d = bench.Dist(world)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d.pg = dist  # (Dist.init would bind a CUDA device)
+    peer = bench.open_peer_exchange(d, lambda: _FakePeer(rank, fail_at), "cpu")
+    q.put((rank, None if peer is None else [h[0] for h in peer.connected]))
+    d.close()
+
+
+@pytest.mark.parametrize("fail_at", [None, ("create", 1), ("connect", 0)])
+def test_peer_exchange_negotiation_is_unanimous(fail_at):
+    """bench.open_peer_exchange: every rank connects with all handles in
+    rank order, or -- if any rank cannot create or connect its block --
+    every rank falls back to the NCCL exchange (no rank left waiting)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_negotiate_worker, args=(world, port, fail_at, q), nprocs=world,
+                       start_method="spawn", join=True)
+    got = dict(q.get(timeout=60) for _ in range(world))
+    if fail_at is None:
+        assert got == {0: [0, 1], 1: [0, 1]}
+    else:
+        assert got == {0: None, 1: None}
