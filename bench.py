@@ -389,6 +389,7 @@ def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int =
 
 
 MM4 = 32768  # config C4
+C4_SAMPLE_ROWS, C4_SAMPLE_COLS = 128, 512  # CPU baseline / parity sample of C
 
 
 def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
@@ -419,6 +420,13 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
     d.barrier()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
+    # rank 0 keeps a 128 x 512 corner of the product (and its operands) for
+    # the CPU baseline and a sampled parity check against the f64 oracle
+    sample = None
+    if d.rank == 0:
+        sample = {"A": A[:C4_SAMPLE_ROWS].cpu().numpy(),
+                  "B": B[:, :C4_SAMPLE_COLS].contiguous().cpu().numpy(),
+                  "C": Cm[:C4_SAMPLE_ROWS, :C4_SAMPLE_COLS].cpu().numpy(), "prec": prec}
     del A, B, ws
     gather_ms = None
     if d.pg is not None:  # the C bands to rank 0, timed apart from the compute
@@ -436,7 +444,8 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
         d.barrier()
     del Cm
     torch.cuda.empty_cache()
-    return {"ms": ms, "rows": nr, "clocks": clk.summary(), "gather_ms": gather_ms}
+    return {"ms": ms, "rows": nr, "clocks": clk.summary(), "gather_ms": gather_ms,
+            "sample": sample}
 
 
 def matmul_device_leg(steps: int, warmup: int) -> dict:
@@ -726,6 +735,29 @@ def cpu_matmul(sample_rows: int = 64) -> dict:
 
 # ----------------------------------------------------------------- main ---
 
+def cpu_matmul_c4(sample: dict) -> dict:
+    """the C4 product is infeasible on the CPU (7e13 flop), so
+    the oracle port times a 128 x 512 corner of it (full K = 32768, every
+    host thread), and the same corner of the GPU's C is checked against the
+    f64 oracle on bf16-rounded operands (tolerance 1e-5 * sum|a||b|)."""
+    from oracle import oracle as O
+    A, B, C = sample["A"], sample["B"], sample["C"]
+    t = time.perf_counter()
+    O.matmul_f32(A, B)
+    s = time.perf_counter() - t
+    prec = {2: O.PREC_BF16, 1: O.PREC_TF32}.get(sample["prec"], O.PREC_F32)
+    Cref, ab = O.matmul_f64(O.round_matrix(prec, A), O.round_matrix(prec, B))
+    err = np.abs(C.astype(np.float64) - Cref)
+    ok = bool(np.all(err <= 1e-5 * ab))
+    return {"value": 2.0 * A.shape[0] * A.shape[1] * B.shape[1] / s / 1e12, "unit": "TFLOP/s",
+            "cores": O.max_threads(), "kind": "port",
+            "sample": f"C[0:{A.shape[0]}, 0:{B.shape[1]}] of the 32768^3 product (full K), "
+                      "oracle/gpcx_oracle.c f32 with every host thread",
+            "parity": {"entries": int(C.size), "within_tolerance": ok,
+                       "max_err_over_bound": float(np.max(err / np.maximum(1e-5 * ab, 1e-300))),
+                       "tolerance": "1e-5 * sum|a||b| vs f64 oracle on bf16-rounded operands"}}
+
+
 def cpu_demosaic(sample_rows: int = 2048, reps: int = 3) -> dict:
     """The REFERENCE's own demosaic (proj/src/demosaic.cpp, compiled from its
     sources into oracle/_ref) on a row band of the bench mosaic, all host
@@ -911,6 +943,8 @@ def run_b200(args) -> None:
             line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
         if dm is not None:
             line["demosaic"]["cpu_baseline"] = cpu_demosaic()
+        if c4 is not None and c4.get("sample") is not None:
+            line["matmul"]["cpu_baseline"] = cpu_matmul_c4(c4["sample"])
     if c5 is not None:
         if d.n == 1:
             c5["cpu_baseline"] = cpu_c5()
