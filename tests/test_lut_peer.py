@@ -82,6 +82,7 @@ def _run_group(tmp_path, nranks, rows, cols, kind, seed, steps, modes):
     (2, 1000, 777, 0),     # ragged band sizes, odd row length
     (2, 4096, 4096, 1),    # uniform16: every bin populated
     (3, 2049, 1024, 0),    # three ranks, uneven split
+    (3, 2, 5, 1),          # rank 2's band is empty: it still meets its peers
 ])
 def test_peer_exchange_equals_single_device_oracle(gpu, tmp_path, nranks, rows, cols, kind):
     from oracle import oracle as O
