@@ -202,3 +202,34 @@ def test_large_requests_overlap_receive_and_match(gpu, server):
     Cref, ab = O.matmul_f64(A, B, rows)
     got = cm.reshape(n, n)[rows.astype(np.int64)].astype(np.float64)
     assert np.all(np.abs(got - Cref) <= 1e-5 * ab + 1e-30)
+
+
+@pytest.mark.gpu
+def test_worker_and_device_count_invariance(gpu, refl):
+    """acceptance.cpp:278-315 pattern (results independent of the worker
+    count), carried to the B200 server: the same requests served with
+    max_tasks 1 and 8, and with the planner splitting large requests into 1
+    or 2 row bands (G.init([0]) / [0, 0]), return byte-identical responses."""
+    from oracle import oracle as O
+    rows, cols = 4096, 4096  # 2^24 px / 2^37 flop: the planner's band thresholds
+    img = O.synth_image(O.IMG_UNIFORM16, 11, rows, cols)
+    m = k = n = 4096
+    A = O.synth_matrix(O.MAT_UNIFORM32, 5, m, k)
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(5), k, n)
+    reqs = [("LUT_CORRECT", f"rows={rows},cols={cols}", img.tobytes()),
+            ("LUT_GEN", f"rows={rows},cols={cols},mode=stretch", img.tobytes()),
+            ("MATMUL", f"m={m},k={k},n={n}", A.tobytes() + B.tobytes()),
+            ("MATMUL", f"m={m},k={k},n={n},prec=bf16", A.tobytes() + B.tobytes())]
+    seen = {}
+    try:
+        for devices in ([0], [0, 0]):
+            G.init(devices)
+            for max_tasks in (1, 8):
+                with G.Server(max_tasks=max_tasks) as s:
+                    for flag, params, payload in reqs:
+                        got = refl.ref_submit(s.port, flag, params, payload, "o.bin")
+                        assert got[0] == "OK", got[:2]
+                        key = (flag, params)
+                        assert seen.setdefault(key, got) == got, (key, devices, max_tasks)
+    finally:
+        G.init([0])
