@@ -233,7 +233,9 @@ int gpcx_lut_correct_peer_device(gpcx_lut_peer* p, const uint16_t* in, uint16_t*
                                  void* stream);
 
 /* C (m x n) = A (m x k) * B (k x n), all f32 row-major with leading
- * dimensions lda/ldb/ldc (elements).  prec selects the path (GPCX_PREC_*). */
+ * dimensions lda/ldb/ldc (elements).  prec selects the path (GPCX_PREC_*).
+ * Workspace: required for TF32 / BF16 (prepared operands); optional for
+ * F32, where it holds A^T for the fastest SIMT kernel (same bits without). */
 int gpcx_matmul_workspace_size(int prec, uint64_t m, uint64_t n, uint64_t k,
                                uint64_t* bytes);
 int gpcx_matmul_device(int prec, uint64_t m, uint64_t n, uint64_t k,

@@ -358,7 +358,8 @@ int gpcx_lut_correct_peer_device(gpcx_lut_peer* p, const uint16_t* in, uint16_t*
 
 int gpcx_matmul_workspace_size(int prec, uint64_t m, uint64_t n, uint64_t k, uint64_t* bytes) {
   return guarded([&] {
-    *bytes = prec == GPCX_PREC_F32 ? 0 : gpcx::gemm::tc_workspace_bytes(prec, m, n, k);
+    *bytes = prec == GPCX_PREC_F32 ? gpcx::gemm::sgemm_workspace_bytes(m, n, k)
+                                   : gpcx::gemm::tc_workspace_bytes(prec, m, n, k);
   });
 }
 
@@ -369,7 +370,8 @@ int gpcx_matmul_device(int prec, uint64_t m, uint64_t n, uint64_t k, const float
     if (lda < k || ldb < n || ldc < n)
       gpcx::fail(gpcx::Errc::BadValue, "leading dimension smaller than the row length");
     if (prec == GPCX_PREC_F32) {
-      gpcx::gemm::launch_sgemm(m, n, k, A, lda, B, ldb, C, ldc, as_stream(stream));
+      // the workspace is optional here (same bits either way, A^T path faster)
+      gpcx::gemm::launch_sgemm(m, n, k, A, lda, B, ldb, C, ldc, ws, ws_bytes, as_stream(stream));
     } else if (prec == GPCX_PREC_TF32 || prec == GPCX_PREC_BF16) {
       need_ws(ws, ws_bytes, gpcx::gemm::tc_workspace_bytes(prec, m, n, k));
       gpcx::gemm::launch_tc(prec, m, n, k, A, lda, B, ldb, C, ldc, ws, as_stream(stream));

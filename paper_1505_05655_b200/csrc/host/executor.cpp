@@ -288,8 +288,11 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
                                     (ks[j + 1] - ks[j]) * row_bytes, s.stream));
     }
     if (p.prec == GPCX_PREC_F32) {
+      const std::uint64_t wsb = gemm::sgemm_workspace_bytes(b.nrows, p.n, p.k);
+      if (wsb != 0) s.mm_ws.ensure(wsb);
       gemm::launch_sgemm(b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,
-                         s.c.as<float>(), p.n, s.stream);
+                         s.c.as<float>(), p.n, wsb != 0 ? s.mm_ws.ptr : nullptr, wsb,
+                         s.stream);
     } else {
       s.mm_ws.ensure(gemm::tc_workspace_bytes(p.prec, b.nrows, p.n, p.k));
       gemm::launch_tc(p.prec, b.nrows, p.n, p.k, s.a.as<float>(), p.k, s.b.as<float>(), p.n,

@@ -133,11 +133,14 @@ void launch_digest(const std::uint16_t* v, std::uint64_t n,
 }  // namespace synth
 
 namespace gemm {
-// SIMT FP32 (reference precision).
+// SIMT FP32 (reference precision).  The workspace (sgemm_workspace_bytes:
+// A^T for aligned shapes, else 0) selects the fastest kernel; without it
+// the same bits come from the row-major-A kernel.
+std::uint64_t sgemm_workspace_bytes(std::uint64_t m, std::uint64_t n, std::uint64_t k);
 void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
                   const float* A, std::uint64_t lda, const float* B,
                   std::uint64_t ldb, float* C, std::uint64_t ldc,
-                  cudaStream_t stream);
+                  void* ws, std::uint64_t ws_bytes, cudaStream_t stream);
 // Tensor-core path (tcgen05): prec = GPCX_PREC_TF32 / GPCX_PREC_BF16.
 std::uint64_t tc_workspace_bytes(int prec, std::uint64_t m, std::uint64_t n,
                                  std::uint64_t k);

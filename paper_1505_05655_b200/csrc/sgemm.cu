@@ -7,7 +7,8 @@
 // plain fp32 FFMA accumulation in a fixed, K-ascending order per output, so
 // results are deterministic and identical for any block-row sharding.
 //
-// sgemm2_kernel (aligned shapes): cp.async multistage, see below.
+// sgemm4_kernel (aligned shapes, workspace for A^T): the default, see below.
+// sgemm2_kernel (aligned shapes, no workspace): cp.async multistage.
 // sgemm_kernel (any shape): 128x128 CTA tile, BK = 8 or 16, 256 threads each owning an 8x8
 // block (2x2 quads of 4x4 so the 128-bit smem reads stay conflict-free), A
 // staged transposed, double-buffered smem with register prefetch of the
@@ -249,6 +250,123 @@ __global__ void __launch_bounds__(THREADS2, MINB)
   }
 }
 
+// ---- A-transposed multistage variant (aligned shapes, with workspace) ---
+// A is transposed once into the workspace (At = A^T, k x m, a 64 x 64 smem
+// transpose: 2 x m x k x 4 bytes of HBM traffic, ~1% of the 4096^3 GEMM),
+// so both operands are MN-major: As[k][m] and Bs[k][n] arrive by 16-byte
+// cp.async with coalesced rows, and per k a thread reads 2 + 2 LDS.128
+// (rows 4 tm + {0..3} and 64 + 4 tm + {0..3}, columns 4 tn + {0..3} and
+// 32 + 4 tn + {0..3}: 64 B of A and 128 B of B per warp, one wavefront
+// each) feeding 32 FFMA2.  Against sgemm2_kernel (A row-major, 8 LDS.128
+// per 4 k over 8 rows) the fragments of one k need 4 loads instead of 10,
+// so the FFMA2 stream starts sooner after each load: 4096^3 53.9 -> 60.0
+// TFLOP/s incl. the transpose (B200, tools/mm_micro.py).  Per output the
+// fma order is still k ascending: bitwise equal to the other kernels.
+__global__ void __launch_bounds__(256)
+    transpose_kernel(const float* __restrict__ A, std::uint64_t lda, std::uint64_t m,
+                     float* __restrict__ At) {
+  // 64 x 64 tile, 16-byte loads and stores (4 of each per thread in flight)
+  __shared__ float t[64][65];
+  const std::uint64_t k0 = static_cast<std::uint64_t>(blockIdx.x) * 64;
+  const std::uint64_t m0 = static_cast<std::uint64_t>(blockIdx.y) * 64;
+  const int r = threadIdx.x >> 4, c4 = (threadIdx.x & 15) * 4;
+  float4 v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    v[i] = *reinterpret_cast<const float4*>(A + (m0 + r + 16 * i) * lda + k0 + c4);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    t[r + 16 * i][c4 + 0] = v[i].x;
+    t[r + 16 * i][c4 + 1] = v[i].y;
+    t[r + 16 * i][c4 + 2] = v[i].z;
+    t[r + 16 * i][c4 + 3] = v[i].w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kr = r + 16 * i;  // row of At (a k), columns m0 + c4 .. + 3
+    *reinterpret_cast<float4*>(At + (k0 + kr) * m + m0 + c4) =
+        make_float4(t[c4 + 0][kr], t[c4 + 1][kr], t[c4 + 2][kr], t[c4 + 3][kr]);
+  }
+}
+
+template <int BK4, int STAGES4>
+constexpr int sgemm4_smem() {
+  return STAGES4 * BK4 * (BM2 + BN2) * 4;
+}
+
+template <int BK4, int STAGES4, int MINB>
+__global__ void __launch_bounds__(THREADS2, MINB)
+    sgemm4_kernel(int m, int k, const float* __restrict__ At, const float* __restrict__ B,
+                  std::uint64_t ldb, float* __restrict__ C, std::uint64_t ldc) {
+  extern __shared__ __align__(16) float smem4[];
+  float (*As)[BK4 * BM2] = reinterpret_cast<float (*)[BK4 * BM2]>(smem4);
+  float (*Bs)[BK4 * BN2] = reinterpret_cast<float (*)[BK4 * BN2]>(smem4 + STAGES4 * BK4 * BM2);
+  const int tid = threadIdx.x;
+  const int tn = tid & 7, tm = tid >> 3;
+  const int m0 = blockIdx.y * BM2, n0 = blockIdx.x * BN2;
+  auto issue = [&](int stage, int k0) {
+#pragma unroll
+    for (int i = 0; i < BK4 / 4; ++i) {  // A^T: BK4 k-rows x 32 chunks of 16 B
+      const int c = tid + THREADS2 * i;
+      const int kr = c >> 5, q = c & 31;
+      cp16(&As[stage][kr * BM2 + 4 * q],
+           At + static_cast<std::uint64_t>(k0 + kr) * static_cast<std::uint64_t>(m) + m0 + 4 * q);
+    }
+#pragma unroll
+    for (int i = 0; i < BK4 / 8; ++i) {  // B: BK4 k-rows x 16 chunks of 16 B
+      const int c = tid + THREADS2 * i;
+      const int kr = c >> 4, q = c & 15;
+      cp16(&Bs[stage][kr * BN2 + 4 * q], B + static_cast<std::uint64_t>(k0 + kr) * ldb + n0 + 4 * q);
+    }
+  };
+  float2 acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) acc[i][p] = make_float2(0.f, 0.f);
+  const int ktiles = k / BK4;
+#pragma unroll
+  for (int st = 0; st < STAGES4 - 1; ++st) {
+    if (st < ktiles) issue(st, st * BK4);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int t = 0; t < ktiles; ++t) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES4 - 2) : "memory");
+    __syncthreads();  // tile t visible; stage (t - 1) % S free to refill
+    const int nt = t + STAGES4 - 1;
+    if (nt < ktiles) issue(nt % STAGES4, nt * BK4);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* as = As[t % STAGES4];
+    const float* bs = Bs[t % STAGES4];
+#pragma unroll
+    for (int kk = 0; kk < BK4; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&as[kk * BM2 + 4 * tm]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&as[kk * BM2 + 64 + 4 * tm]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&bs[kk * BN2 + 4 * tn]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&bs[kk * BN2 + 32 + 4 * tn]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                           make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[i][p] = __ffma2_rn(ai, b[p], acc[i][p]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = m0 + (i < 4 ? 4 * tm + i : 64 + 4 * tm + (i - 4));
+    float* crow = C + static_cast<std::uint64_t>(row) * ldc + n0;
+    *reinterpret_cast<float4*>(crow + 4 * tn) =
+        make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+    *reinterpret_cast<float4*>(crow + 32 + 4 * tn) =
+        make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+  }
+}
+
 bool sgemm2_fits(std::uint64_t m, std::uint64_t n, std::uint64_t k, const float* A,
                  std::uint64_t lda, const float* B, std::uint64_t ldb, const float* C,
                  std::uint64_t ldc) {
@@ -279,10 +397,17 @@ void launch_variant(std::uint64_t m, std::uint64_t n, std::uint64_t k, const flo
 
 }  // namespace
 
+std::uint64_t sgemm_workspace_bytes(std::uint64_t m, std::uint64_t n, std::uint64_t k) {
+  // A^T for sgemm4_kernel (aligned shapes; the pointers are checked at launch)
+  const bool shape_ok = m % BM2 == 0 && n % BN2 == 0 && k % 64 == 0 && m > 0 && n > 0 &&
+                        m <= 0x7FFFFFFFull && k <= 0x7FFFFFFFull && (m / BM2) <= 65535;
+  return shape_ok ? m * k * 4 : 0;
+}
+
 void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
                   const float* A, std::uint64_t lda, const float* B,
                   std::uint64_t ldb, float* C, std::uint64_t ldc,
-                  cudaStream_t stream) {
+                  void* ws, std::uint64_t ws_bytes, cudaStream_t stream) {
   if (m == 0 || n == 0) return;
   if (m > 0x7FFFFFFFull || n > 0x7FFFFFFFull || k > 0x7FFFFFFFull)
     fail(Errc::TooLarge, "matmul dimension exceeds 2^31");
@@ -294,7 +419,30 @@ void launch_sgemm(std::uint64_t m, std::uint64_t n, std::uint64_t k,
   }
   const char* v = std::getenv("GPCX_SGEMM");
   const std::string variant = v != nullptr ? v : "";
-  if ((variant.empty() || variant[0] == 'c') && sgemm2_fits(m, n, k, A, lda, B, ldb, C, ldc)) {
+  const std::uint64_t at_bytes = sgemm_workspace_bytes(m, n, k);
+  if ((variant.empty() || variant[0] == 't') && at_bytes != 0 && ws != nullptr &&
+      ws_bytes >= at_bytes && (reinterpret_cast<std::uintptr_t>(ws) & 15u) == 0 &&
+      sgemm2_fits(m, n, k, A, lda, B, ldb, C, ldc)) {
+    auto* at = static_cast<float*>(ws);
+    transpose_kernel<<<dim3(static_cast<unsigned>(k / 64), static_cast<unsigned>(m / 64)), 256, 0,
+                       stream>>>(A, lda, m, at);
+    GPCX_LAUNCH_CHECK();
+    const dim3 grid(static_cast<unsigned>(n / BN2), static_cast<unsigned>(m / BM2));
+    auto go = [&](auto kernel, int smem) {
+      GPCX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kernel<<<grid, THREADS2, smem, stream>>>(static_cast<int>(m), static_cast<int>(k), at, B,
+                                               ldb, C, ldc);
+    };
+    // GPCX_SGEMM=t32x3 | t16x4 for A/B runs
+    if (variant == "t32x3") go(sgemm4_kernel<32, 3, 2>, sgemm4_smem<32, 3>());
+    else if (variant == "t16x4") go(sgemm4_kernel<16, 4, 2>, sgemm4_smem<16, 4>());
+    else go(sgemm4_kernel<16, 3, 2>, sgemm4_smem<16, 3>());
+    GPCX_LAUNCH_CHECK();
+    return;
+  }
+  // no workspace (or GPCX_SGEMM=c...): A read row-major by sgemm2_kernel
+  if ((variant.empty() || variant[0] == 'c' || variant[0] == 't') &&
+      sgemm2_fits(m, n, k, A, lda, B, ldb, C, ldc)) {
     const dim3 grid(static_cast<unsigned>(n / BN2), static_cast<unsigned>(m / BM2));
     auto go = [&](auto kernel, int smem) {
       GPCX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -88,6 +88,27 @@ def test_sgemm_strided_operands(gpu):
     assert float(big_c[:, 160:].abs().max()) == 0.0
 
 
+@pytest.mark.parametrize("m,n,k", [(256, 384, 512), (1024, 640, 192)])
+def test_sgemm_kernels_agree_bitwise(gpu, monkeypatch, m, n, k):
+    """The three SIMT kernels -- A^T (with workspace), row-major A (without),
+    register-staged (GPCX_SGEMM=8x2) -- fma-accumulate each output over k in
+    ascending order, so they must agree bit for bit."""
+    import torch
+    from paper_1505_05655_b200 import device as D
+    A, B = _mats(O.MAT_UNIFORM32, 21, m, k, n)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ws = D.matmul_workspace(O.PREC_F32, m, n, k)
+    assert ws is not None and ws.numel() == m * k * 4
+    outs = []
+    for variant, w in (("", ws), ("", None), ("8x2", None)):
+        monkeypatch.setenv("GPCX_SGEMM", variant)
+        dC = torch.full((m, n), float("nan"), device="cuda")
+        D.matmul(O.PREC_F32, dA, dB, dC, w)
+        outs.append(dC.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    _check(outs[0], A, B, O.PREC_F32)
+
+
 def test_sgemm_c2_size_sampled(gpu):
     """Config C2 (4096^3, f32) checked on 64 sampled rows."""
     A, B = _mats(O.MAT_UNIFORM32, 0x5EED, 4096, 4096, 4096)

@@ -40,7 +40,7 @@ def main():
         A = D.synth_matrix(1, 1, 4096, 4096)
         B = D.synth_matrix(1, 2, 4096, 4096)
         Cm = torch.empty(4096, 4096, device="cuda")
-        D.matmul(0, A, B, Cm)
+        D.matmul(0, A, B, Cm, D.matmul_workspace(0, 4096, 4096, 4096))
         torch.cuda.synchronize()
     if "demosaic" in args.what:  # BAYER_BILINEAR / BAYER_GRADIENT at 16384^2
         img = D.synth_image(1, 3, 16384, 16384)
