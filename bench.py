@@ -672,7 +672,35 @@ def c1_leg(n_gpus: int) -> dict:
         G.init([0])
     res["workload"] = ("C1: one LUT_CORRECT request (4096^2 u16, equalize) at a time through the "
                        "B200 server, loopback TCP, median latency")
+    res["direct"] = c1_direct(imgs[0])
     return res
+
+
+def c1_direct(img: bytes, reps: int = 20) -> dict:
+    """The same C1 request through the task-level C ABI (gpcx_run) from
+    pinned host buffers -- the server's work without the sockets: 32 MiB
+    H2D, the fused LUT kernel, 32 MiB D2H."""
+    import ctypes as C
+    import paper_1505_05655_b200 as G
+    n = C5_IMG * C5_IMG
+    pin, pout = G.lib.gpcx_pinned_alloc(2 * n), G.lib.gpcx_pinned_alloc(2 * n)
+    try:
+        src = np.ctypeslib.as_array((C.c_uint16 * n).from_address(pin))
+        src[:] = np.frombuffer(img, dtype=np.uint16)
+        dst = np.ctypeslib.as_array((C.c_uint8 * (2 * n)).from_address(pout))
+        ts = []
+        for i in range(reps + 2):
+            t = time.perf_counter()
+            G.run("LUT_CORRECT", f"rows={C5_IMG},cols={C5_IMG},mode=equalize", src, dst)
+            if i >= 2:
+                ts.append(time.perf_counter() - t)
+    finally:
+        G.lib.gpcx_pinned_free(pin)
+        G.lib.gpcx_pinned_free(pout)
+    ms = statistics.median(ts) * 1e3
+    return {"ms_per_request": round(ms, 3), "Gpixel/s": round(n / ms / 1e6, 3),
+            "h2d_bytes": 2 * n, "d2h_bytes": 2 * n,
+            "path": "gpcx_run LUT_CORRECT, pinned host buffers, median of 20"}
 
 
 # -------------------------------------------------------------- CPU legs ---
@@ -700,6 +728,17 @@ def cpu_c1() -> dict:
         res = c1_run(rs.port, imgs[0], reps=5, warmup=1)
     res.update({"kind": "port", "cores": O.max_threads(),
                 "sample": "5 sequential requests after 1 warm-up, same image and client"})
+    px = np.frombuffer(imgs[0], dtype=np.uint16)
+    ts = []
+    for i in range(6):
+        t = time.perf_counter()
+        O.lut_correct(px, O.LUT_EQUALIZE)
+        if i:
+            ts.append(time.perf_counter() - t)
+    ms = statistics.median(ts) * 1e3
+    res["direct"] = {"ms_per_request": round(ms, 3), "Gpixel/s": round(px.size / ms / 1e6, 3),
+                     "path": "oracle/gpcx_oracle.c LUT_CORRECT in process, every host thread, "
+                             "median of 5"}
     return res
 
 
