@@ -1037,6 +1037,101 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------- gpc bench, GPU columns ---
+
+def _median_ms(run, reps: int = 5) -> float:
+    """gpc.cpp:243-254: median of 5 wall-clock runs."""
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        run()
+        ts.append((time.perf_counter() - t) * 1e3)
+    return sorted(ts)[len(ts) // 2]
+
+
+def _gpu_median_ms(run, reps: int = 5) -> float:
+    import torch
+    run()  # warm-up (lazy allocations, attributes)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        run()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[len(ts) // 2]
+
+
+def run_gpc_bench(args) -> None:
+    """`gpc bench` (proj/tools/gpc.cpp:256-370) with the GPU columns SURVEY.md
+    §8 a12 asks for: per task and worker count the reference's serial and
+    parallel CPU times (the reference's own kernels from oracle/_ref for
+    BAYER_*, the restated oracle for LUT_CORRECT / MATMUL), then the B200
+    kernel on one GPU (device-resident, CUDA events, median of 5), its
+    throughput and roofline fraction.  TSV on stdout."""
+    import torch
+    from oracle import oracle as O
+    from paper_1505_05655_b200 import device as D
+    pk = peaks()
+    task = args.task
+    hw = len(os.sched_getaffinity(0))
+    workers = [int(w) for w in (args.workers_list or f"1,{hw}").split(",")]
+    cols = ["task", "config", "workers", "serial_ms", "parallel_ms", "speedup", "gpus", "gpu_ms",
+            "gpu_speedup", "throughput", "unit", "roofline_frac"]
+    print("\t".join(cols))
+    rng = np.random.default_rng(0x5EED)
+
+    def row(config, w, serial, parallel, gpu_ms, thr, unit, frac):
+        print("\t".join([task, config, str(w), f"{serial:.3f}", f"{parallel:.3f}",
+                         f"{serial / parallel:.2f}", "1", f"{gpu_ms:.4f}", f"{serial / gpu_ms:.1f}",
+                         f"{thr:.2f}", unit, f"{frac:.3f}"]), flush=True)
+
+    if task in ("BAYER_BILINEAR", "BAYER_GRADIENT"):
+        rows, cols_ = (int(x) for x in (args.dims or "2048x2048").split("x"))
+        grad = task == "BAYER_GRADIENT"
+        img = rng.integers(0, 1 << 16, rows * cols_, dtype=np.uint16)
+        serial = _median_ms(lambda: O.ref_demosaic(grad, img, rows, cols_, gpcref=True))
+        dimg = torch.from_numpy(img.view(np.int16)).cuda()
+        out = torch.empty(3 * rows * cols_, dtype=torch.int16, device="cuda")
+        gms = _gpu_median_ms(lambda: D.demosaic(grad, 0, dimg, rows, cols_, out))
+        thr = rows * cols_ / gms / 1e6
+        frac = 8.0 * rows * cols_ / (gms / 1e3) / 1e9 / pk["hbm_gbs"]
+        for w in workers:
+            par = _median_ms(lambda: O.ref_demosaic(grad, img, rows, cols_, workers=w))
+            row(f"{rows}x{cols_}", w, serial, par, gms, thr, "Gpixel/s", frac)
+    elif task == "LUT_CORRECT":
+        rows, cols_ = (int(x) for x in (args.dims or "4096x4096").split("x"))
+        img = O.synth_image(O.IMG_RAMP12, SEED, rows, cols_)
+        serial = _median_ms(lambda: O.lut_correct(img, O.LUT_EQUALIZE, threads=1))
+        dimg = D.synth_image(0, SEED, rows, cols_)
+        out = torch.empty_like(dimg)
+        lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(dimg.numel())
+        gms = _gpu_median_ms(lambda: D.lut_correct(dimg, out, O.LUT_EQUALIZE, lut, stats, ws))
+        thr = rows * cols_ / gms / 1e6
+        frac = 6.0 * rows * cols_ / (gms / 1e3) / 1e9 / pk["hbm_gbs"]
+        for w in workers:
+            par = _median_ms(lambda: O.lut_correct(img, O.LUT_EQUALIZE, threads=w))
+            row(f"{rows}x{cols_}/equalize", w, serial, par, gms, thr, "Gpixel/s", frac)
+    elif task == "MATMUL":
+        m = k = n = int(args.dims or 1024)
+        A = O.synth_matrix(O.MAT_UNIFORM32, SEED, m, k)
+        B = O.synth_matrix(O.MAT_UNIFORM32, SEED_B, k, n)
+        serial = _median_ms(lambda: O.matmul_f32(A, B, threads=1), reps=3)
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        dC = torch.empty(m, n, device="cuda")
+        for prec, name in ((0, "f32"), (2, "bf16")):
+            ws = D.matmul_workspace(prec, m, n, k)
+            gms = _gpu_median_ms(lambda: D.matmul(prec, dA, dB, dC, ws))
+            tf = 2.0 * m * n * k / gms / 1e9
+            peak = 74.4 if prec == 0 else (pk["bf16_tflops_sustained"] or pk["bf16_tflops"])
+            for w in workers:
+                par = _median_ms(lambda: O.matmul_f32(A, B, threads=w), reps=3)
+                row(f"{m}^3/prec={name}", w, serial, par, gms, tf, "TFLOP/s", tf / peak)
+    else:
+        raise SystemExit("--task must be BAYER_BILINEAR, BAYER_GRADIENT, LUT_CORRECT or MATMUL")
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1044,9 +1139,17 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=["all", "lut", "matmul", "c5", "demosaic"], default="all")
+    # `gpc bench` mode (TSV, proj/tools/gpc.cpp:256-370 + GPU columns)
+    ap.add_argument("--gpc-bench", action="store_true")
+    ap.add_argument("--task", default="LUT_CORRECT")
+    ap.add_argument("--dims", default="")
+    ap.add_argument("--workers-list", default="")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpc_bench:
+        run_gpc_bench(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

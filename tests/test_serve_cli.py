@@ -57,3 +57,22 @@ def test_serves_then_drains_on_signal(gpu, refl, sig):
         if p.poll() is None:
             p.kill()
             p.communicate()
+
+
+@pytest.mark.gpu
+def test_gpc_bench_mode_prints_reference_columns_plus_gpu(gpu, refl):
+    """bench.py --gpc-bench: `gpc bench`'s TSV (task, config, workers,
+    serial_ms, parallel_ms, speedup; proj/tools/gpc.cpp:256-370) extended
+    with gpus, gpu_ms, gpu_speedup, throughput, unit, roofline_frac."""
+    import sys
+    root = BIN.parent.parent.parent
+    for task, dims in (("LUT_CORRECT", "512x768"), ("BAYER_GRADIENT", "256x256"), ("MATMUL", "256")):
+        r = subprocess.run([sys.executable, "bench.py", "--gpc-bench", "--task", task, "--dims", dims,
+                            "--workers-list", "1,2"], cwd=root, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [l.split("\t") for l in r.stdout.strip().splitlines()]
+        assert lines[0] == ["task", "config", "workers", "serial_ms", "parallel_ms", "speedup",
+                            "gpus", "gpu_ms", "gpu_speedup", "throughput", "unit", "roofline_frac"]
+        assert len(lines) == 1 + (4 if task == "MATMUL" else 2)
+        assert all(l[0] == task and float(l[7]) > 0 for l in lines[1:])
