@@ -237,7 +237,7 @@ def open_peer_exchange(d: Dist, make_peer, dev):
     return peer
 
 
-def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
+def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int, gather: bool = True) -> dict:
     import torch
     from paper_1505_05655_b200 import device as D
     dev = torch.device("cuda", d.gpu)
@@ -305,7 +305,7 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int) -> dict:
     # here; the oracle check of this exact band runs in the cpu leg).
     dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
     st = D.read_stats(stats)
-    gather_ms = gather_leg(d, out) if d.pg is not None else None
+    gather_ms = gather_leg(d, out) if d.pg is not None and gather else None
     if peer is not None:
         d.barrier()  # no rank unmaps its exchange block while a peer may still read it
         torch.cuda.synchronize()
@@ -829,6 +829,10 @@ def run_b200(args) -> None:
     d.init("nccl")
     mode = 0
     lut = lut_device_leg(d, args.steps, args.warmup, mode)
+    # the other LUT mode (contrast stretch): min/max instead of a histogram
+    # at N=1 (read-only reduction, no atomics); the same exchange at N>1
+    stretch = lut_device_leg(d, args.steps, args.warmup, 1, gather=False)
+    stretch_ms = d.max(stretch["ms"])
     ms = d.max(lut["ms"])
     exch_ms = d.max(lut["exch_ms"]) if lut["exch_ms"] is not None else None
     hist_ms = d.max(lut["hist_ms"])
@@ -839,7 +843,7 @@ def run_b200(args) -> None:
     if args.workload in ("all", "demosaic") and d.rank == 0:
         torch.cuda.empty_cache()
         dm = demosaic_leg(max(3, min(args.steps, 10)), 3)
-    mm = c4 = None
+    mm = c4 = c4_tf32 = None
     if args.workload in ("all", "matmul"):
         torch.cuda.empty_cache()
         # C2 before C4: right after the 1 kW C4 GEMMs the power controller
@@ -848,6 +852,9 @@ def run_b200(args) -> None:
             mm = matmul_device_leg(max(3, min(args.steps, 10)), 2)
         d.barrier()
         c4 = matmul_c4_leg(d, max(2, min(args.steps, 5)), 1)
+        # the TF32 tensor-core path on the same C4 problem (kind::tf32)
+        c4_tf32 = matmul_c4_leg(d, 2, 1, prec=1)
+        c4_tf32["ms_max"] = d.max(c4_tf32["ms"])
         c4["ms_max"] = d.max(c4["ms"])
         if c4["gather_ms"] is not None:
             c4["gather_ms"] = d.max(c4["gather_ms"])
@@ -907,6 +914,17 @@ def run_b200(args) -> None:
             "clocks": lut["clocks"]}
     if gather is not None:
         line["gather"] = gather
+    st_ach = 6.0 * band_px / (stretch_ms / args.steps / 1e3) / 1e9
+    line["stretch"] = {
+        "workload": "C3 with mode=stretch (LUT from the global min/max)",
+        "value": round(px_total * args.steps / (stretch_ms / 1e3) / 1e9, 2), "unit": "Gpixel/s",
+        "ms_per_step": round(stretch_ms / args.steps, 4),
+        "kernels": ("lut::minmax_kernel (2 B/px, redux.sync min/max) + from_minmax + apply_kernel "
+                    "(4 B/px)" if d.n == 1 else "fused_kernel with the peer exchange, as equalize"),
+        "roofline": {"bound": "hbm", "achieved": round(st_ach, 1), "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(st_ach / pk["hbm_gbs"], 4),
+                     "algorithmic_bytes_per_step": 6 * band_px},
+        "clocks": stretch["clocks"]}
     # e2e first among the host-heavy legs: the C5 / C1 TCP traffic and the
     # CPU baselines load the host memory system the PCIe copies share
     e2e_steps = max(4, min(args.steps, 8))
@@ -947,6 +965,18 @@ def run_b200(args) -> None:
         if c4["gather_ms"] is not None:
             line["matmul"]["gather"] = {"ms": round(c4["gather_ms"], 3), "bytes": 4 * MM4 * MM4,
                                         "what": "C bands (f32) gathered to rank 0, not in `value`"}
+        if c4_tf32 is not None:
+            tf32 = flops / (c4_tf32["ms_max"] / 1e3) / 1e12
+            line["matmul"]["tf32"] = {
+                "workload": "C4 with prec=tf32 (tcgen05 kind::tf32, operands rounded RNA)",
+                "value": round(tf32, 1), "unit": "TFLOP/s", "ms_per_step": round(c4_tf32["ms_max"], 3),
+                "tolerance": "|c-c_ref| <= 1e-5 * sum|a||b| vs f64 oracle on tf32-rounded operands",
+                "roofline": {"bound": "tensor", "achieved": round(tf32, 1),
+                             "peak": round((pk["bf16_tflops_sustained"] or pk["bf16_tflops"]) / 2, 1),
+                             "unit": "TFLOP/s",
+                             "peak_note": "half the measured sustained bf16 rate (dense tf32 = 1/2 bf16)",
+                             "frac": round(tf32 / ((pk["bf16_tflops_sustained"] or pk["bf16_tflops"]) / 2), 4)},
+                "clocks": c4_tf32["clocks"]}
     if mm is not None:
         mm_line = {"workload": "C2: MATMUL prec=f32 (SIMT, reference precision), 4096^3",
                    "value": round(mm["tflops"], 2),
