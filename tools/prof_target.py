@@ -36,6 +36,14 @@ def main():
         D.lut_apply(lut, img, out)  # LUT_APPLY's kernel on the same scene
         torch.cuda.synchronize()
         del img, out
+    if "stretch" in args.what:  # C3 scene, mode=stretch: minmax + from_minmax + apply
+        n = 32768 * 32768
+        img = D.synth_image(0, 0x5EED, 32768, 32768)
+        out = torch.empty_like(img)
+        lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+        D.lut_correct(img, out, 1, lut, stats, ws)
+        torch.cuda.synchronize()
+        del img, out
     if "sgemm" in args.what:  # config C2: FP32 SIMT 4096^3
         A = D.synth_matrix(1, 1, 4096, 4096)
         B = D.synth_matrix(1, 2, 4096, 4096)
