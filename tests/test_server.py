@@ -233,3 +233,68 @@ def test_worker_and_device_count_invariance(gpu, refl):
                         assert seen.setdefault(key, got) == got, (key, devices, max_tasks)
     finally:
         G.init([0])
+
+
+def _raw_exchange(port: int, request: bytes) -> bytes:
+    with socket.create_connection(("127.0.0.1", port), timeout=10) as s:
+        s.sendall(request)
+        s.shutdown(socket.SHUT_WR)
+        chunks = []
+        while True:
+            b = s.recv(65536)
+            if not b:
+                break
+            chunks.append(b)
+    return b"".join(chunks)
+
+
+def _malformed(i: int, rng) -> bytes:
+    """acceptance.cpp:529-627's ten malformed-request classes (plus the
+    B200 flags for the classes that apply to them)."""
+    flag = ["BAYER_BILINEAR", "LUT_CORRECT", "MATMUL"][i // 10 % 3]
+    case = i % 10
+    if case == 0:
+        return W.header("DEVINFO", "", "out.bin", marker=0x5A)
+    if case == 1:
+        return W.header("DEVINFO", "", "", marker=W.MARK_DATA)
+    if case == 2:
+        return W.header(flag, "rows=64,cols=64" if flag != "MATMUL" else "m=4,k=4,n=4", "x.raw",
+                        marker=W.MARK_NONE)
+    if case == 3:
+        return W.header(f"NO_SUCH_TASK_{rng.randrange(1000)}", "", "", marker=W.MARK_NONE)
+    if case == 4:
+        return W.header(flag, "rows=1048576,cols=1048576" if flag != "MATMUL"
+                        else "m=1048576,k=1048576,n=1048576", "", marker=W.MARK_DATA)
+    if case == 5:
+        h = bytearray(W.header(flag, "", "", marker=W.MARK_NONE))
+        h[20] = ord("X")
+        return bytes(h)
+    if case == 6:
+        h = bytearray(W.header("DEVINFO", "a=b", "", marker=W.MARK_NONE))
+        h[31] = 0x01
+        return bytes(h)
+    if case == 7:
+        return W.header(flag, "rows=8,rows=9,cols=8", "", marker=W.MARK_DATA)
+    if case == 8:
+        return W.header(flag, "==,,", "", marker=W.MARK_DATA)
+    return W.header(flag, "rows=abc,cols=8" if flag != "MATMUL" else "m=abc,k=2,n=2", "",
+                    marker=W.MARK_DATA)
+
+
+def test_malformed_request_fuzz_over_tcp(server, refl):
+    """acceptance.cpp:529-627 over loopback TCP: every malformed request gets
+    a well-formed ERR frame -- byte-identical to the reference server's for
+    the reference's own flags -- and the server keeps serving."""
+    import random
+    rng = random.Random(0xBADF00D5)
+    with refl.RefServer() as rs:
+        for i in range(300):
+            req = _malformed(i, rng)
+            ours = _raw_exchange(server.port, req)
+            r = W.parse_response(ours)
+            assert r["status"].startswith("ERR:"), (i, r["status"])
+            flag = req[:29].split(b"\0", 1)[0]
+            if not flag.startswith((b"LUT_", b"MATMUL")):
+                assert ours == _raw_exchange(rs.port, req), (i, r["status"])
+    status, _, _, _ = refl.ref_submit(server.port, "NOPE", "", b"", "a")
+    assert status == "ERR:UNKNOWN_TASK"
