@@ -121,13 +121,26 @@ __device__ __forceinline__ uint4 pack8(const std::uint32_t (&p)[8]) {
 template <int RPT>
 constexpr int kMinBlocks = 4;
 
-template <bool kGradient, int kDc, int RPT>
+// A band of output rows [row_base, row_base + out_rows) of a rows x cols
+// mosaic: `in` holds image rows [in_row0, ...) (the band plus its 1-row
+// halo, or the whole image), `out` three band-local planes of out_rows x
+// cols.  Edge clamp and CFA parity use image coordinates, so a band equals
+// the same rows of the whole-image result.
+template <bool kGradient, int kDc, int RPT, bool kBand>
 __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
     demosaic_kernel(const std::uint16_t* __restrict__ in, std::uint16_t* __restrict__ out,
-                    int rows, int cols, int dr, int vec_ok) {
+                    int rows, int cols, int dr, int vec_ok, int band_row_base, int band_in_row0,
+                    int band_out_rows) {
+  // whole image (kBand false): the band arguments fold to constants, so the
+  // hot single-device kernel keeps its register budget (64, no spills)
+  const int row_base = kBand ? band_row_base : 0;
+  const int in_row0 = kBand ? band_in_row0 : 0;
+  const int out_rows = kBand ? band_out_rows : rows;
   constexpr int TR = 8 * RPT;
   __shared__ __align__(16) std::uint16_t tile[TR + 2][SW];
-  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
+  const int r0 = row_base + blockIdx.y * TR, c0 = blockIdx.x * TC;
+  const int row_end = row_base + out_rows;
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // Stage the tile: row i of the tile is image row clamp(r0 - 1 + i).
@@ -135,32 +148,36 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
   // (rows and halo columns) are issued before the first smem store, so they
   // are in flight together.
   constexpr int kRowsPerWarp = (TR + 2 + THREADS / 32 - 1) / (THREADS / 32);
+  constexpr int kBatch = 5;  // rows in flight per warp (64-row tiles: 5 + 4)
   const bool full_cols = vec_ok && c0 + TC <= cols;
   if (full_cols) {
-    uint4 q[kRowsPerWarp];
-    std::uint32_t halo[kRowsPerWarp];
 #pragma unroll
-    for (int j = 0; j < kRowsPerWarp; ++j) {
-      const int i = warp + j * (THREADS / 32);
-      if (i < TR + 2) {
-        const int gr = min(max(r0 - 1 + i, 0), rows - 1);
-        const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr) * cols;
-        q[j] = __ldg(reinterpret_cast<const uint4*>(grow + c0) + lane);
-        if (lane < 2) halo[j] = __ldg(grow + (lane == 0 ? max(c0 - 1, 0) : min(c0 + TC, cols - 1)));
+    for (int j0 = 0; j0 < kRowsPerWarp; j0 += kBatch) {
+      uint4 q[kBatch];
+      std::uint32_t halo[kBatch];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const int i = warp + (j0 + j) * (THREADS / 32);
+        if (j0 + j < kRowsPerWarp && i < TR + 2) {
+          const int gr = min(max(r0 - 1 + i, 0), rows - 1);
+          const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr - in_row0) * cols;
+          q[j] = __ldg(reinterpret_cast<const uint4*>(grow + c0) + lane);
+          if (lane < 2) halo[j] = __ldg(grow + (lane == 0 ? max(c0 - 1, 0) : min(c0 + TC, cols - 1)));
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < kRowsPerWarp; ++j) {
-      const int i = warp + j * (THREADS / 32);
-      if (i < TR + 2) {
-        reinterpret_cast<uint4*>(tile[i] + kPad)[lane] = q[j];
-        if (lane < 2) tile[i][lane == 0 ? kPad - 1 : kPad + TC] = static_cast<std::uint16_t>(halo[j]);
+      for (int j = 0; j < kBatch; ++j) {
+        const int i = warp + (j0 + j) * (THREADS / 32);
+        if (j0 + j < kRowsPerWarp && i < TR + 2) {
+          reinterpret_cast<uint4*>(tile[i] + kPad)[lane] = q[j];
+          if (lane < 2) tile[i][lane == 0 ? kPad - 1 : kPad + TC] = static_cast<std::uint16_t>(halo[j]);
+        }
       }
     }
   } else {
     for (int i = warp; i < TR + 2; i += THREADS / 32) {
       const int gr = min(max(r0 - 1 + i, 0), rows - 1);
-      const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr) * cols;
+      const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr - in_row0) * cols;
       std::uint16_t* srow = tile[i];
       for (int c = lane; c < TC; c += 32) srow[kPad + c] = grow[min(c0 + c, cols - 1)];
       if (lane == 0) srow[kPad - 1] = grow[max(c0 - 1, 0)];
@@ -169,7 +186,7 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
   }
   __syncthreads();
 
-  const std::uint64_t plane = static_cast<std::uint64_t>(rows) * cols;
+  const std::uint64_t plane = static_cast<std::uint64_t>(out_rows) * cols;
   const int ty = warp, tx = lane;
   const int x0 = kPad + 8 * tx;
   const int col0 = c0 + 8 * tx;
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
 #pragma unroll
   for (int rr = 0; rr < RPT; ++rr) {
     const int row = r0 + RPT * ty + rr;
-    if (row >= rows) break;
+    if (row >= row_end) break;
     if (rr >= 1) rw[rr + 2] = load_row(tile[RPT * ty + rr + 2], x0);
     std::uint32_t pr[8], pg[8], pb[8];
     // row parity is warp-uniform (a warp owns one row pair)
@@ -192,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
       mosaic_row<kGradient, true, kDc>(rw[rr], rw[rr + 1], rw[rr + 2], pr, pg, pb);
     else
       mosaic_row<kGradient, false, kDc>(rw[rr], rw[rr + 1], rw[rr + 2], pr, pg, pb);
-    const std::uint64_t off = static_cast<std::uint64_t>(row) * cols + col0;
+    const std::uint64_t off = static_cast<std::uint64_t>(row - row_base) * cols + col0;
     if (vec_ok && col0 + 8 <= cols) {
       __stcs(reinterpret_cast<uint4*>(out + off), pack8(pr));
       __stcs(reinterpret_cast<uint4*>(out + plane + off), pack8(pg));
@@ -211,16 +228,20 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
 
 }  // namespace
 
-void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
-            std::uint64_t rows, std::uint64_t cols, cudaStream_t stream) {
+void launch_band(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
+                 std::uint64_t rows, std::uint64_t cols, std::uint64_t row_base,
+                 std::uint64_t in_row0, std::uint64_t out_rows, cudaStream_t stream) {
   if (rows < 2 || cols < 2)
     fail(Errc::BadImage, "image is " + std::to_string(rows) + "x" + std::to_string(cols) +
                              ", need at least 2x2");
   if (rows > 0x7FFFFFFFull || cols > 0x7FFFFFFFull) fail(Errc::TooLarge, "image too large");
+  if (row_base + out_rows > rows || in_row0 > (row_base > 0 ? row_base - 1 : 0))
+    fail(Errc::BadValue, "band outside the image or missing its halo row");
+  if (out_rows == 0) return;
   // phase: 0 RGGB (0,0), 1 BGGR (1,1), 2 GRBG (0,1), 3 GBRG (1,0)
   static const int kDr[4] = {0, 1, 0, 1}, kDc[4] = {0, 1, 1, 0};
   const int dr = kDr[phase & 3], dc = kDc[phase & 3];
-  const std::uint64_t plane = rows * cols;
+  const std::uint64_t plane = out_rows * cols;
   // 128-bit paths need every row and every plane to start 16-byte aligned.
   const int vec_ok = (cols % 8 == 0) && (plane % 8 == 0) &&
                      (((reinterpret_cast<std::uintptr_t>(out) | reinterpret_cast<std::uintptr_t>(in)) & 15) == 0);
@@ -234,14 +255,29 @@ void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* ou
   }();
   const int rpt = rpt_env != 0 ? rpt_env : (gradient ? 8 : 4);
   const std::uint64_t tr = 8u * rpt;
-  const dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC), static_cast<unsigned>((rows + tr - 1) / tr));
+  const dim3 grid(static_cast<unsigned>((cols + TC - 1) / TC),
+                  static_cast<unsigned>((out_rows + tr - 1) / tr));
   if (grid.y > 65535) fail(Errc::TooLarge, "too many rows for the tile grid");
-  auto kernel = rpt == 8 ? (gradient ? (dc ? demosaic_kernel<true, 1, 8> : demosaic_kernel<true, 0, 8>)
-                                     : (dc ? demosaic_kernel<false, 1, 8> : demosaic_kernel<false, 0, 8>))
-                         : (gradient ? (dc ? demosaic_kernel<true, 1, 4> : demosaic_kernel<true, 0, 4>)
-                                     : (dc ? demosaic_kernel<false, 1, 4> : demosaic_kernel<false, 0, 4>));
-  kernel<<<grid, THREADS, 0, stream>>>(in, out, (int)rows, (int)cols, dr, vec_ok);
+  const bool band = row_base != 0 || in_row0 != 0 || out_rows != rows;
+  auto pick = [&](auto whole, auto banded) { return band ? banded : whole; };
+  auto kernel =
+      rpt == 8
+          ? (gradient ? (dc ? pick(demosaic_kernel<true, 1, 8, false>, demosaic_kernel<true, 1, 8, true>)
+                            : pick(demosaic_kernel<true, 0, 8, false>, demosaic_kernel<true, 0, 8, true>))
+                      : (dc ? pick(demosaic_kernel<false, 1, 8, false>, demosaic_kernel<false, 1, 8, true>)
+                            : pick(demosaic_kernel<false, 0, 8, false>, demosaic_kernel<false, 0, 8, true>)))
+          : (gradient ? (dc ? pick(demosaic_kernel<true, 1, 4, false>, demosaic_kernel<true, 1, 4, true>)
+                            : pick(demosaic_kernel<true, 0, 4, false>, demosaic_kernel<true, 0, 4, true>))
+                      : (dc ? pick(demosaic_kernel<false, 1, 4, false>, demosaic_kernel<false, 1, 4, true>)
+                            : pick(demosaic_kernel<false, 0, 4, false>, demosaic_kernel<false, 0, 4, true>)));
+  kernel<<<grid, THREADS, 0, stream>>>(in, out, (int)rows, (int)cols, dr, vec_ok, (int)row_base,
+                                       (int)in_row0, (int)out_rows);
   GPCX_LAUNCH_CHECK();
+}
+
+void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
+            std::uint64_t rows, std::uint64_t cols, cudaStream_t stream) {
+  launch_band(gradient, phase, in, out, rows, cols, 0, 0, rows, stream);
 }
 
 }  // namespace gpcx::demosaic

@@ -308,16 +308,34 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
 void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
                 std::uint16_t* out) {
   const InflightGuard inflight;
-  rt::Runtime& R = rt::Runtime::get();
-  rt::SlotLease lease = R.acquire(R.pick_device_index());
-  rt::Slot& s = *lease;
   const std::uint64_t n = p.rows * p.cols;
-  s.a.ensure(n * 2);
-  s.c.ensure(n * 6);
-  rt::h2d(s, s.a.ptr, in, n * 2);
-  demosaic::launch(gradient, p.phase, s.a.as<std::uint16_t>(), s.c.as<std::uint16_t>(), p.rows,
-                   p.cols, s.stream);
-  rt::d2h(s, out, s.c.ptr, n * 6);
+  if (p.rows < 2 || p.cols < 2)  // BayerImage::validate, before any staging
+    demosaic::launch(gradient, p.phase, nullptr, nullptr, p.rows, p.cols, nullptr);
+  // Large mosaics split into row bands over the bound devices (SURVEY §8f
+  // row 1): band i stages its rows plus the 1-row halo above and below,
+  // computes its rows with image-coordinate clamp / parity, and DMAs its
+  // three band-local planes into the three plane slices of the response.
+  const std::vector<Band> bands = plan_bands(p.rows, n, kShardMinPixels);
+  rt::Runtime& R = rt::Runtime::get();
+  std::vector<rt::SlotLease> leases;
+  leases.reserve(bands.size());
+  for (const Band& b : bands) leases.push_back(R.acquire(b.dev_index));
+  const std::uint64_t plane = n;
+  for_each_band(bands.size(), [&](std::size_t i) {
+    rt::Slot& s = *leases[i];
+    rt::use_device(s.device);
+    const Band& b = bands[i];
+    const std::uint64_t in0 = b.row0 > 0 ? b.row0 - 1 : 0;
+    const std::uint64_t in1 = std::min(p.rows, b.row0 + b.nrows + 1);
+    const std::uint64_t bn = b.nrows * p.cols;
+    s.a.ensure((in1 - in0) * p.cols * 2);
+    s.c.ensure(bn * 6);
+    rt::h2d(s, s.a.ptr, in + in0 * p.cols, (in1 - in0) * p.cols * 2);
+    demosaic::launch_band(gradient, p.phase, s.a.as<std::uint16_t>(), s.c.as<std::uint16_t>(),
+                          p.rows, p.cols, b.row0, in0, b.nrows, s.stream);
+    for (int k = 0; k < 3; ++k)  // R, G, B planes of the band
+      rt::d2h(s, out + k * plane + b.row0 * p.cols, s.c.as<std::uint16_t>() + k * bn, bn * 2);
+  });
 }
 
 void lsq_host(const task::LsqParams& p, const void* y, double* out) {

@@ -106,6 +106,12 @@ namespace demosaic {
 // (RGGB, BGGR, GRBG, GBRG).  BadImage below 2x2 like BayerImage::validate.
 void launch(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
             std::uint64_t rows, std::uint64_t cols, cudaStream_t stream);
+// Output rows [row_base, row_base + out_rows) into three band-local planes
+// (out_rows x cols each); `in` holds image rows from in_row0 on, which must
+// include the band's halo rows (in_row0 <= max(row_base - 1, 0)).
+void launch_band(bool gradient, int phase, const std::uint16_t* in, std::uint16_t* out,
+                 std::uint64_t rows, std::uint64_t cols, std::uint64_t row_base,
+                 std::uint64_t in_row0, std::uint64_t out_rows, cudaStream_t stream);
 }  // namespace demosaic
 
 namespace lsq {

@@ -212,3 +212,25 @@ def test_both_tile_heights_equal_reference(gpu, refl, rpt):
     r = subprocess.run([sys.executable, "-c", _RPT_CHECK], cwd=root, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bands,rows,cols,phase", [
+    (2, 4096, 4096, "RGGB"),
+    (3, 4099, 4104, "GBRG"),   # uneven bands, odd band starts
+    (2, 4100, 4097, "BGGR"),   # odd row length: the scalar store path
+])
+def test_row_band_sharded_demosaic_equals_reference(gpu, refl, bands, rows, cols, phase):
+    """The planner splits large mosaics into row bands (1-row halo each side,
+    image-coordinate clamp and CFA parity); the served result must equal the
+    reference's whole-image kernel byte for byte."""
+    rng = np.random.default_rng(rows ^ cols)
+    img = _mosaic(rng, rows, cols)
+    try:
+        G.init([0] * bands)
+        for flag, grad in (("BAYER_BILINEAR", False), ("BAYER_GRADIENT", True)):
+            _, out = G.run(flag, f"rows={rows},cols={cols},phase={phase}", img)
+            ref = refl.ref_demosaic(grad, img, rows, cols, phase, workers=0)
+            assert np.array_equal(out.view(np.uint16), ref), (flag, bands)
+    finally:
+        G.init([0])
