@@ -56,8 +56,10 @@ def _run_device(prec, A, B):
     return dC.cpu().numpy()
 
 
-SHAPES = [(128, 128, 16), (256, 384, 512), (1, 1, 1), (3, 5, 7), (129, 130, 131), (1000, 17, 300),
-          (64, 1024, 4096)]
+# (256, 384, 512): A^T SIMT kernel; (256, 128, 96): k % 64 != 0 -> row-major-A
+# kernel; ragged shapes -> the register-staged kernel
+SHAPES = [(128, 128, 16), (256, 384, 512), (256, 128, 96), (1, 1, 1), (3, 5, 7), (129, 130, 131),
+          (1000, 17, 300), (64, 1024, 4096)]
 
 
 @pytest.mark.parametrize("m,n,k", SHAPES)
