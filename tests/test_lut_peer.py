@@ -20,6 +20,22 @@ import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 
+
+@pytest.fixture(scope="module")
+def shared_gpu(gpu):
+    """The ranks are separate processes on cuda:0: needs the Default compute
+    mode (an exclusive-process GPU admits one context)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        mode = pynvml.nvmlDeviceGetComputeMode(pynvml.nvmlDeviceGetHandleByIndex(0))
+        pynvml.nvmlShutdown()
+    except Exception:
+        return gpu
+    if mode != 0:  # NVML_COMPUTEMODE_DEFAULT
+        pytest.skip(f"compute mode {mode}: one process per GPU only")
+    return gpu
+
 _WORKER = r"""
 import json, os, sys, time
 from pathlib import Path
@@ -84,7 +100,7 @@ def _run_group(tmp_path, nranks, rows, cols, kind, seed, steps, modes):
     (3, 2049, 1024, 0),    # three ranks, uneven split
     (3, 2, 5, 1),          # rank 2's band is empty: it still meets its peers
 ])
-def test_peer_exchange_equals_single_device_oracle(gpu, tmp_path, nranks, rows, cols, kind):
+def test_peer_exchange_equals_single_device_oracle(shared_gpu, tmp_path, nranks, rows, cols, kind):
     from oracle import oracle as O
     steps, modes = 4, [O.LUT_EQUALIZE, O.LUT_EQUALIZE, O.LUT_STRETCH, O.LUT_EQUALIZE]
     res = _run_group(tmp_path, nranks, rows, cols, kind, 0x5EED, steps, modes)
@@ -139,7 +155,7 @@ os._exit(code)
 
 
 @pytest.mark.gpu
-def test_peer_rank_without_peers_traps_instead_of_hanging(gpu, tmp_path):
+def test_peer_rank_without_peers_traps_instead_of_hanging(shared_gpu, tmp_path):
     """A group of 2 where rank 1 connects but never launches: rank 0's
     kernel must trap after GPCX_PEER_TIMEOUT_MS and the failure must surface
     on its stream (a dead peer never hangs the GPU)."""
