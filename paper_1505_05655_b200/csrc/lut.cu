@@ -71,41 +71,174 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
                : "memory");
 }
 
-// Count one sample into the packed smem histogram.  Word w holds bin 2w in
-// its low half and bin 2w+1 in its high half, so the word equals
-// count(2w) + 65536*count(2w+1) mod 2^32.  The thread whose atomic wraps a
-// half sees it in the returned old value and books the lost 65536 (and, for
-// a low-half carry into the high half, the spurious +1) into the global
+// Packed smem histogram: logical word w holds bin 2w in its low half and
+// bin 2w+1 in its high half, so the word equals count(2w) +
+// 65536*count(2w+1) mod 2^32.
+//
+// Bank layout.  Values with trailing zero bits -- MSB-aligned 8 / 10 / 12
+// bit sensor data, multiples of 2^k -- put every lane of a warp on the same
+// bank (8-bit data x 128: 7.4 ms instead of 1.2 at 32768^2).  Such images
+// use the swizzled layout: word w at physical word swz(w), which XORs bits
+// 5-9 and 10-14 into the bank bits 0-4 (a bijection that only permutes the
+// words of each 32-word group, and its own inverse).  The LUT staged in
+// smem for the apply pass uses the same layout.  The choice is made per
+// launch from a fixed sample of the image (`prefers_swizzle`); it changes
+// only where counts live, never their values.
+__device__ __host__ __forceinline__ uint32_t swz(uint32_t w) {
+  return w ^ (((w >> 5) ^ (w >> 10)) & 31u);
+}
+template <bool kSwz>
+__device__ __forceinline__ uint32_t word_of(uint32_t v) {
+  return kSwz ? swz(v >> 1) : (v >> 1);
+}
+
+// Add k (<= 65535) samples of value v.  The thread whose atomic wraps a
+// half sees it in the returned old value and books the lost 65536 (and,
+// for a low-half carry into the high half, the spurious +1) into the global
 // overflow counters; the merge adds them back mod 2^32.  Exact for any
 // count < 2^32 and independent of the interleaving.
-__device__ __forceinline__ void count_one(uint32_t* bins,
-                                          uint32_t* overflow,
-                                          uint32_t v) {
+template <bool kSwz>
+__device__ __forceinline__ void count_k(uint32_t* bins, uint32_t* overflow, uint32_t v,
+                                        uint32_t k) {
   const uint32_t hi_bin = v & 1u;
-  const uint32_t inc = hi_bin ? 0x10000u : 1u;
-  const uint32_t mask = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
-  const uint32_t old = atomicAdd(&bins[v >> 1], inc);
-  if ((old & mask) == mask) {
+  const uint32_t old = atomicAdd(&bins[word_of<kSwz>(v)], hi_bin ? k << 16 : k);
+  const uint32_t half = hi_bin ? old >> 16 : old & 0xFFFFu;
+  if (half + k > 0xFFFFu) {
     atomicAdd(&overflow[v], 65536u);
     if (!hi_bin) {
       // carry into the high half: +1 there that is not a sample of v+1,
       // and possibly a wrap of the high half itself.
-      atomicAdd(&overflow[v + 1],
-                (old >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
+      atomicAdd(&overflow[v + 1], (old >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
     }
   }
 }
 
-__device__ __forceinline__ void count_vec(uint32_t* bins,
-                                          uint32_t* overflow, uint4 q) {
-  count_one(bins, overflow, q.x & 0xFFFFu);
-  count_one(bins, overflow, q.x >> 16);
-  count_one(bins, overflow, q.y & 0xFFFFu);
-  count_one(bins, overflow, q.y >> 16);
-  count_one(bins, overflow, q.z & 0xFFFFu);
-  count_one(bins, overflow, q.z >> 16);
-  count_one(bins, overflow, q.w & 0xFFFFu);
-  count_one(bins, overflow, q.w >> 16);
+template <bool kSwz>
+__device__ __forceinline__ void count_one(uint32_t* bins, uint32_t* overflow, uint32_t v) {
+  const uint32_t hi_bin = v & 1u;
+  const uint32_t inc = hi_bin ? 0x10000u : 1u;
+  const uint32_t mask = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+  const uint32_t old = atomicAdd(&bins[word_of<kSwz>(v)], inc);
+  if ((old & mask) == mask) {
+    atomicAdd(&overflow[v], 65536u);
+    if (!hi_bin)
+      atomicAdd(&overflow[v + 1], (old >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
+  }
+}
+
+// 8 samples per lane: the 8 returning atomics are issued back to back and
+// their (rare) wrap checks OR-ed into one branch per vector.  Checking each
+// result right after its atomic serialised the 8 latencies, which is what
+// made repetitive data slow: on one word the lanes' returning atomics
+// queue up (constant 32768^2: 4.47 -> 1.27 ms; two-level 2.88 -> 2.40).
+template <bool kSwz>
+__device__ __forceinline__ void count_vec_plain(uint32_t* bins,
+                                                uint32_t* overflow, uint4 q) {
+  const uint32_t v[8] = {q.x & 0xFFFFu, q.x >> 16, q.y & 0xFFFFu, q.y >> 16,
+                         q.z & 0xFFFFu, q.z >> 16, q.w & 0xFFFFu, q.w >> 16};
+  uint32_t old[8];
+  bool wrapped = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t hi_bin = v[j] & 1u;
+    const uint32_t m = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+    old[j] = atomicAdd(&bins[word_of<kSwz>(v[j])], hi_bin ? 0x10000u : 1u);
+    wrapped |= (old[j] & m) == m;
+  }
+  if (wrapped) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t hi_bin = v[j] & 1u;
+      const uint32_t m = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+      if ((old[j] & m) != m) continue;
+      atomicAdd(&overflow[v[j]], 65536u);
+      if (!hi_bin)
+        atomicAdd(&overflow[v[j] + 1], (old[j] >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
+    }
+  }
+}
+
+// Repetitive data (flat regions, binary or few-level images): on one word
+// the lanes' returning atomics queue up, so a warp whose samples fall on
+// few banks combines them first -- one atomic for a flat warp vector
+// (k = 8 x active lanes), else one per distinct value (__match_any_sync).
+template <bool kSwz>
+__device__ __noinline__ void count_vec_few(uint32_t* bins, uint32_t* overflow, uint4 q,
+                                           uint32_t mask) {
+  const uint32_t v[8] = {q.x & 0xFFFFu, q.x >> 16, q.y & 0xFFFFu, q.y >> 16,
+                         q.z & 0xFFFFu, q.z >> 16, q.w & 0xFFFFu, q.w >> 16};
+  const uint32_t lane = threadIdx.x & 31u;
+  const int leader = __ffs(mask) - 1;
+  const uint32_t pair = v[0] | (v[0] << 16);
+  const bool flat = (q.x == pair) & (q.y == pair) & (q.z == pair) & (q.w == pair);
+  const uint32_t lead_v = __shfl_sync(mask, v[0], leader);  // every lane of mask
+  if (__all_sync(mask, flat & (v[0] == lead_v))) {
+    if (lane == static_cast<uint32_t>(leader)) count_k<kSwz>(bins, overflow, v[0], 8u * __popc(mask));
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t peers = __match_any_sync(mask, v[j]);
+    if (lane == static_cast<uint32_t>(__ffs(peers) - 1))
+      count_k<kSwz>(bins, overflow, v[j], __popc(peers));
+  }
+}
+
+// Few distinct words among the warp's first samples of the vectors?
+template <bool kSwz>
+__device__ __forceinline__ uint32_t bank_bit(uint4 q) {
+  return 1u << (word_of<kSwz>(q.x & 0xFFFFu) & 31u);
+}
+
+template <bool kSwz>
+__device__ __forceinline__ void count_vec(uint32_t* bins, uint32_t* overflow, uint4 q) {
+  const uint32_t mask = __activemask();
+  if (__popc(__reduce_or_sync(mask, bank_bit<kSwz>(q))) <= 4) count_vec_few<kSwz>(bins, overflow, q, mask);
+  else count_vec_plain<kSwz>(bins, overflow, q);
+}
+
+// The main loop's two vectors share one probe (half its cost per sample).
+template <bool kSwz>
+__device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, uint4 q0,
+                                           uint4 q1) {
+  const uint32_t mask = __activemask();
+  if (__popc(__reduce_or_sync(mask, bank_bit<kSwz>(q0) | bank_bit<kSwz>(q1))) <= 6) {
+    count_vec_few<kSwz>(bins, overflow, q0, mask);
+    count_vec_few<kSwz>(bins, overflow, q1, mask);
+  } else {
+    count_vec_plain<kSwz>(bins, overflow, q0);
+    count_vec_plain<kSwz>(bins, overflow, q1);
+  }
+}
+
+// Per-launch choices from a fixed sample -- 256 pairs of adjacent samples
+// spread over the image, the same in every CTA:
+//   bit 0  swizzled layout: the OR of the samples has >= 3 trailing zero
+//          bits, i.e. the image looks MSB-aligned;
+//   bit 1  repetitive data: >= 1/8 of the pairs are equal (flat regions,
+//          binary or few-level images; noise-free ramps too) -> the count
+//          pass probes each warp's diversity and combines equal values.
+//          Ordinary images skip that probe (it costs ~2.5% on them).
+// Warp 0 computes the flags into *flags; the caller's next __syncthreads
+// publishes them.  They change where and how counts are added, never what.
+__device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uint64_t n,
+                                              uint32_t* flags) {
+  if (threadIdx.x >= 32) return;
+  uint32_t o = 0, eq = 0;
+  if (n >= 2) {
+    for (uint32_t i = threadIdx.x; i < 256; i += 32) {
+      const std::uint64_t p = (static_cast<std::uint64_t>(i) * (n - 2)) / 255;
+      const uint32_t a = img[p], b = img[p + 1];
+      o |= a | b;
+      eq += a == b;
+    }
+  } else if (n == 1 && threadIdx.x == 0) {
+    o = img[0];
+  }
+  o = __reduce_or_sync(0xFFFFFFFFu, o);
+  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
+  if (threadIdx.x == 0)
+    *flags = ((n != 0 && (o & 7u) == 0) ? 1u : 0u) | (eq >= 32 ? 2u : 0u);
 }
 
 // Samples before the first 16-byte boundary (pointers are at least 2-byte
@@ -117,18 +250,40 @@ __device__ __host__ __forceinline__ std::uint64_t head_len(const void* p,
   return h < n ? h : n;
 }
 
+// LUT entry v of the smem LUT (u16 entries, two per word; swizzled words
+// when kSwz -- see the bank layout note above).
+template <bool kSwz>
+__device__ __forceinline__ uint32_t lut_at(const std::uint16_t* s_lut, uint32_t v) {
+  return kSwz ? s_lut[(swz(v >> 1) << 1) | (v & 1u)] : s_lut[v];
+}
+
+template <bool kSwz>
 __device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
   uint4 r;
-  r.x = s_lut[q.x & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.x >> 16]) << 16);
-  r.y = s_lut[q.y & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.y >> 16]) << 16);
-  r.z = s_lut[q.z & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.z >> 16]) << 16);
-  r.w = s_lut[q.w & 0xFFFFu] | (static_cast<uint32_t>(s_lut[q.w >> 16]) << 16);
+  r.x = lut_at<kSwz>(s_lut, q.x & 0xFFFFu) | (lut_at<kSwz>(s_lut, q.x >> 16) << 16);
+  r.y = lut_at<kSwz>(s_lut, q.y & 0xFFFFu) | (lut_at<kSwz>(s_lut, q.y >> 16) << 16);
+  r.z = lut_at<kSwz>(s_lut, q.z & 0xFFFFu) | (lut_at<kSwz>(s_lut, q.z >> 16) << 16);
+  r.w = lut_at<kSwz>(s_lut, q.w & 0xFFFFu) | (lut_at<kSwz>(s_lut, q.w >> 16) << 16);
   return r;
+}
+
+// Stage the global LUT (logical order) into smem in the kSwz layout.
+template <bool kSwz>
+__device__ __forceinline__ void stage_lut(uint4* smem, const std::uint16_t* lut_g) {
+  if constexpr (kSwz) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(lut_g);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(smem);
+    for (int w = threadIdx.x; w < kWords; w += blockDim.x) dst[swz(w)] = __ldcg(src + w);
+  } else {
+    const uint4* src = reinterpret_cast<const uint4*>(lut_g);
+    for (int i = threadIdx.x; i < kBins / 8; i += blockDim.x) smem[i] = __ldcg(src + i);
+  }
 }
 
 // Histogram of img[0, n) into the packed smem bins; CTA `cta` of `ctas`
 // (grid-stride over 128-bit vectors, two-vector software pipeline: the next
 // stage's loads are in flight while this stage's 16 samples are counted).
+template <bool kSwz, bool kFew>
 __device__ __forceinline__ void count_image(const std::uint16_t* img,
                                             std::uint64_t n, int cta, int ctas,
                                             uint32_t* bins, uint32_t* overflow) {
@@ -136,10 +291,10 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t tail0 = head + (nvec << 3);
   if (cta == 0)
-    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one(bins, overflow, img[i]);
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one<kSwz>(bins, overflow, img[i]);
   if (cta == ctas - 1)
     for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
-      count_one(bins, overflow, img[i]);
+      count_one<kSwz>(bins, overflow, img[i]);
   const uint4* body = reinterpret_cast<const uint4*>(img + head);
   const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
   std::uint64_t i = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
@@ -156,19 +311,27 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
       nq[0] = ld_stream(body + nx);
       nq[1] = ld_stream(body + nx + stride);
     }
-    count_vec(bins, overflow, q[0]);
-    count_vec(bins, overflow, q[1]);
+    if constexpr (kFew) {
+      count_pair<kSwz>(bins, overflow, q[0], q[1]);
+    } else {
+      count_vec_plain<kSwz>(bins, overflow, q[0]);
+      count_vec_plain<kSwz>(bins, overflow, q[1]);
+    }
     q[0] = nq[0];
     q[1] = nq[1];
     i = nx;
     have = nhave;
   }
-  for (; i < nvec; i += stride) count_vec(bins, overflow, ld_stream(body + i));
+  for (; i < nvec; i += stride) {
+    if constexpr (kFew) count_vec<kSwz>(bins, overflow, ld_stream(body + i));
+    else count_vec_plain<kSwz>(bins, overflow, ld_stream(body + i));
+  }
 }
 
 // out = LUT[in] over [0, n) with the LUT in smem; CTA `cta` of `ctas`.
 // Two vectors per stage, the next stage's loads in flight while this one is
 // looked up and stored (tools/apply_bench.cu: = cudaMemcpy D2D bandwidth).
+template <bool kSwz>
 __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const std::uint16_t* in,
                                             std::uint16_t* out, std::uint64_t n, int cta,
                                             int ctas) {
@@ -177,8 +340,8 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
   const std::uint64_t head = head_len(in, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t tail0 = head + (nvec << 3);
-  if (tid < head) out[tid] = s_lut[in[tid]];
-  if (tid < n - tail0) out[tail0 + tid] = s_lut[in[tail0 + tid]];
+  if (tid < head) out[tid] = lut_at<kSwz>(s_lut, in[tid]);
+  if (tid < n - tail0) out[tail0 + tid] = lut_at<kSwz>(s_lut, in[tail0 + tid]);
   const uint4* src = reinterpret_cast<const uint4*>(in + head);
   uint4* dst = reinterpret_cast<uint4*>(out + head);
   constexpr int kU = 2;
@@ -197,13 +360,13 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
       for (int u = 0; u < kU; ++u) nq[u] = ld_stream(src + nx + u * stride);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) st_stream(dst + i + u * stride, lookup_vec(s_lut, q[u]));
+    for (int u = 0; u < kU; ++u) st_stream(dst + i + u * stride, lookup_vec<kSwz>(s_lut, q[u]));
 #pragma unroll
     for (int u = 0; u < kU; ++u) q[u] = nq[u];
     i = nx;
     have = nhave;
   }
-  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec(s_lut, ld_stream(src + i)));
+  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec<kSwz>(s_lut, ld_stream(src + i)));
 }
 
 // floor(num / d) for num < 2^50 and d >= 1 without a 64-bit integer divide
@@ -348,11 +511,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   LUT_STAMP(0);
   const bool count = stages & kCount;
+  // smem layout of this launch (the same in every CTA: a fixed sample of img)
+  __shared__ uint32_t s_swz;
+  if ((stages & (kCount | kApply)) != 0) sample_layout(img, n, &s_swz);
+  if (!count) __syncthreads();  // else published by the zeroing's barrier
   // ---- phase 1: per-CTA histograms
   if (count && static_cast<int>(blockIdx.x) < nparts) {
     for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    count_image(img, n, blockIdx.x, nparts, bins, overflow);
+    switch (s_swz & 3u) {
+      case 0: count_image<false, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 1: count_image<true, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 2: count_image<false, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      default: count_image<true, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+    }
     __syncthreads();
     LUT_STAMP(1);
     uint4* dst = reinterpret_cast<uint4*>(parts + static_cast<std::uint64_t>(blockIdx.x) * kWords);
@@ -361,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(2);
   if (count) grid.sync();
   LUT_STAMP(3);
+  const bool swizzled = (s_swz & 1u) != 0;  // published by a barrier above (read only with img)
 
   // ---- phase 2: merge this CTA's 512-bin slice
   const bool slice_cta = static_cast<int>(blockIdx.x) < kSlices;
@@ -387,9 +560,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = 0; u < 8; ++u) add(x[u]);
       }
       for (; p < nparts; p += kGroups) add(__ldcg(pq + p * kPartQuads));
-      // red[group][bin], bin = 8 * quad + j of the slice
+      // red[group][bin], bin = 8 * quad + j of the slice -- logical bins:
+      // in the swizzled layout the quad's physical words 4 quad .. +3 hold
+      // logical words swz(.)
+      if (swizzled) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t pw = blockIdx.x * 256u + quad * 4u + (j >> 1);
+          bins[group * 512 + 2 * (swz(pw) - blockIdx.x * 256u) + (j & 1)] = acc[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bins[group * 512 + quad * 8 + j] = acc[j];
+      }
     }
     __syncthreads();
     const bool exchange = stages & kExchange;
@@ -528,14 +711,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(7);
 
   // ---- phase 4: apply
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(lut);
-    for (int i = t; i < kBins / 8; i += kThreads) smem_u4[i] = __ldcg(src + i);
-  }
+  if (swizzled) stage_lut<true>(smem_u4, lut);
+  else stage_lut<false>(smem_u4, lut);
   __syncthreads();
   LUT_STAMP(8);
-  apply_image(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
-              gridDim.x);
+  if (swizzled)
+    apply_image<true>(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
+                      gridDim.x);
+  else
+    apply_image<false>(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
+                       gridDim.x);
 #ifdef GPCX_LUT_TRACE
   __syncthreads();
 #endif
@@ -646,19 +831,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
                  int vector_ok) {
   extern __shared__ uint4 smem_u4[];
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(lut_g);
-    for (int i = threadIdx.x; i < kBins / 8; i += kThreads) smem_u4[i] = src[i];
-  }
+  __shared__ uint32_t s_swz;
+  sample_layout(in, n, &s_swz);
+  __syncthreads();
+  const bool swizzled = (s_swz & 1u) != 0;
+  if (swizzled) stage_lut<true>(smem_u4, lut_g);
+  else stage_lut<false>(smem_u4, lut_g);
   __syncthreads();
   const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
   if (!vector_ok) {  // mismatched alignment of in/out: scalar path
     const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
     for (std::uint64_t i = tid; i < n; i += static_cast<std::uint64_t>(gridDim.x) * kThreads)
-      out[i] = s_lut[in[i]];
+      out[i] = swizzled ? lut_at<true>(s_lut, in[i]) : lut_at<false>(s_lut, in[i]);
     return;
   }
-  apply_image(s_lut, in, out, n, blockIdx.x, gridDim.x);
+  if (swizzled) apply_image<true>(s_lut, in, out, n, blockIdx.x, gridDim.x);
+  else apply_image<false>(s_lut, in, out, n, blockIdx.x, gridDim.x);
 }
 
 bool g_attrs_set[64] = {};

@@ -298,3 +298,81 @@ def test_task_errors_map_to_errc(gpu):
     with pytest.raises(G.GpcxError) as e:
         G.run("LUT_CORRECT", "rows=4,cols=4,mode=log", np.zeros(16, dtype=np.uint16))
     assert e.value.code == "BadValue"
+
+
+@pytest.mark.parametrize("shift", [4, 6, 8])
+@pytest.mark.parametrize("rows,cols", [(333, 517), (2048, 4096)])
+def test_msb_aligned_images_bit_exact(gpu, shift, rows, cols):
+    """MSB-aligned sensor data (12 / 10 / 8 significant bits shifted up):
+    every value has trailing zero bits, so the kernels use the swizzled smem
+    layout for the histogram and the staged LUT -- histogram, fused
+    LUT_CORRECT and the standalone LUT_APPLY kernel must stay bit-exact."""
+    torch, D = _dev()
+    rng = np.random.default_rng(shift * 1000 + rows)
+    vals = ((rng.integers(0, 1 << 16, rows * cols, dtype=np.uint32) >> shift) << shift).astype(np.uint16)
+    img = torch.from_numpy(vals.view(np.int16)).to(gpu)
+    hist = torch.zeros(65536, dtype=torch.int32, device=gpu)
+    ws = D.lut_workspace(img.numel())
+    D.lut_hist(img, hist, ws)
+    assert np.array_equal(hist.cpu().numpy().view(np.uint32).astype(np.uint64), O.lut_hist(vals))
+    for mode, _ in MODES:
+        out = torch.empty_like(img)
+        lut, stats = D.new_lut(), D.new_stats()
+        D.lut_correct(img, out, mode, lut, stats, ws)
+        r_out, r_lut, r_st = O.lut_correct(vals, mode)
+        assert np.array_equal(u16(out), r_out) and np.array_equal(u16(lut), r_lut), mode
+        assert D.read_stats(stats) == r_st
+        out2 = torch.empty_like(img)
+        D.lut_apply(lut, img, out2)
+        assert np.array_equal(u16(out2), r_out)
+
+
+def test_swizzled_and_flat_counter_wraps(gpu):
+    """Counts far past 65535 per CTA in the swizzled layout (few MSB-aligned
+    values, combined per warp) and in flat runs (one atomic per warp vector,
+    k = 8 x active lanes), including runs that end mid-vector and mid-warp."""
+    torch, D = _dev()
+    n = 4_000_003
+    vals = np.empty(n, dtype=np.uint16)
+    vals[0::3] = 0x1000
+    vals[1::3] = 0x2000
+    vals[2::3] = 0xF000
+    vals[: n // 2] = np.where(np.arange(n // 2) % 97 < 90, 0x4000, vals[: n // 2])  # flat runs
+    img = torch.from_numpy(vals.view(np.int16)).to(gpu)
+    ref_out, ref_lut, ref_st = O.lut_correct(vals, O.LUT_EQUALIZE)
+    hist = torch.zeros(65536, dtype=torch.int32, device=gpu)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    for _ in range(2):  # the overflow counters must come back zeroed
+        D.lut_hist(img, hist, ws)
+        assert np.array_equal(hist.cpu().numpy().view(np.uint32).astype(np.uint64), O.lut_hist(vals))
+        out = torch.empty_like(img)
+        D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+        assert np.array_equal(u16(out), ref_out) and np.array_equal(u16(lut), ref_lut)
+        assert D.read_stats(stats) == ref_st
+
+
+@pytest.mark.parametrize("variant", ["plain", "plain_swizzled", "few", "few_swizzled"])
+def test_counter_wraps_every_count_variant(gpu, variant):
+    """Each of the four count-pass variants (smem layout plain / swizzled x
+    repetitive-data probe off / on, picked per launch from a fixed sample)
+    with > 65535 samples of a value per CTA, so the packed u16 halves wrap."""
+    torch, D = _dev()
+    n = 24_000_007  # 2 values over 148 CTAs: ~81K samples of each per CTA
+    base = np.array([0x3000, 0x3008] if "swizzled" in variant else [1000, 1001], dtype=np.uint16)
+    if variant.startswith("plain"):
+        vals = base[np.arange(n) % 2]               # adjacent samples always differ
+    else:
+        vals = base[(np.arange(n) // 37) % 2]       # runs of 37: repetitive
+    img = torch.from_numpy(vals.view(np.int16)).to(gpu)
+    hist = torch.zeros(65536, dtype=torch.int32, device=gpu)
+    ws = D.lut_workspace(n)
+    ref_h = O.lut_hist(vals)
+    assert ref_h.min(where=ref_h > 0, initial=n) > 148 * 65536  # > 65535 per value per CTA
+    D.lut_hist(img, hist, ws)
+    assert np.array_equal(hist.cpu().numpy().view(np.uint32).astype(np.uint64), ref_h)
+    ref_out, ref_lut, ref_st = O.lut_correct(vals, O.LUT_EQUALIZE)
+    out = torch.empty_like(img)
+    lut, stats = D.new_lut(), D.new_stats()
+    D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+    assert np.array_equal(u16(out), ref_out) and np.array_equal(u16(lut), ref_lut)
+    assert D.read_stats(stats) == ref_st
