@@ -226,11 +226,21 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
   if (threadIdx.x >= 32) return;
   uint32_t o = 0, eq = 0;
   if (n >= 2) {
-    for (uint32_t i = threadIdx.x; i < 256; i += 32) {
-      const std::uint64_t p = (static_cast<std::uint64_t>(i) * (n - 2)) / 255;
-      const uint32_t a = img[p], b = img[p + 1];
-      o |= a | b;
-      eq += a == b;
+    // 8 pairs per lane, all 16 loads in flight at once (this runs while
+    // the other warps zero the histogram, and C1's whole kernel is ~40 us)
+    const double step = static_cast<double>(n - 2) / 255.0;
+    uint32_t a[8], b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const std::uint64_t p =
+          static_cast<std::uint64_t>(static_cast<double>(threadIdx.x + 32 * k) * step);
+      a[k] = __ldg(img + p);
+      b[k] = __ldg(img + p + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      o |= a[k] | b[k];
+      eq += a[k] == b[k];
     }
   } else if (n == 1 && threadIdx.x == 0) {
     o = img[0];
