@@ -82,7 +82,7 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 // 5-9 and 10-14 into the bank bits 0-4 (a bijection that only permutes the
 // words of each 32-word group, and its own inverse).  The LUT staged in
 // smem for the apply pass uses the same layout.  The choice is made per
-// launch from a fixed sample of the image (`prefers_swizzle`); it changes
+// launch from a fixed sample of the image (`sample_layout`); it changes
 // only where counts live, never their values.
 __device__ __host__ __forceinline__ uint32_t swz(uint32_t w) {
   return w ^ (((w >> 5) ^ (w >> 10)) & 31u);
@@ -127,10 +127,9 @@ __device__ __forceinline__ void count_one(uint32_t* bins, uint32_t* overflow, ui
 }
 
 // 8 samples per lane: the 8 returning atomics are issued back to back and
-// their (rare) wrap checks OR-ed into one branch per vector.  Checking each
-// result right after its atomic serialised the 8 latencies, which is what
-// made repetitive data slow: on one word the lanes' returning atomics
-// queue up (constant 32768^2: 4.47 -> 1.27 ms; two-level 2.88 -> 2.40).
+// their (rare) wrap checks OR-ed into one branch per vector instead of a
+// branch (and its reconvergence pair) after each atomic -- C3 step 1.211 ->
+// 1.195 ms.
 template <bool kSwz>
 __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
                                                 uint32_t* overflow, uint4 q) {
