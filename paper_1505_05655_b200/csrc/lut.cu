@@ -159,8 +159,9 @@ __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
 
 // Repetitive data (flat regions, binary or few-level images): on one word
 // the lanes' returning atomics queue up, so a warp whose samples fall on
-// few banks combines them first -- one atomic for a flat warp vector
-// (k = 8 x active lanes), else one per distinct value (__match_any_sync).
+// few banks combines them first -- one or two atomics when the warp vector
+// holds at most two values (flat / binary: warp min, max and a count),
+// else one per distinct value per sample slot (__match_any_sync).
 template <bool kSwz>
 __device__ __noinline__ void count_vec_few(uint32_t* bins, uint32_t* overflow, uint4 q,
                                            uint32_t mask) {
@@ -168,11 +169,38 @@ __device__ __noinline__ void count_vec_few(uint32_t* bins, uint32_t* overflow, u
                          q.z & 0xFFFFu, q.z >> 16, q.w & 0xFFFFu, q.w >> 16};
   const uint32_t lane = threadIdx.x & 31u;
   const int leader = __ffs(mask) - 1;
+  // flat warp vector: one atomic
   const uint32_t pair = v[0] | (v[0] << 16);
   const bool flat = (q.x == pair) & (q.y == pair) & (q.z == pair) & (q.w == pair);
   const uint32_t lead_v = __shfl_sync(mask, v[0], leader);  // every lane of mask
   if (__all_sync(mask, flat & (v[0] == lead_v))) {
     if (lane == static_cast<uint32_t>(leader)) count_k<kSwz>(bins, overflow, v[0], 8u * __popc(mask));
+    return;
+  }
+  // at most two values (binary): the warp's min and max, and how many
+  // samples equal the min -- two atomics in all
+  uint32_t mn = v[0], mx = v[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) {
+    mn = min(mn, v[j]);
+    mx = max(mx, v[j]);
+  }
+  mn = __reduce_min_sync(mask, mn);
+  mx = __reduce_max_sync(mask, mx);
+  bool two = true;
+  uint32_t c_mn = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    two &= (v[j] == mn) | (v[j] == mx);
+    c_mn += v[j] == mn;
+  }
+  if (__all_sync(mask, two)) {
+    c_mn = __reduce_add_sync(mask, c_mn);
+    if (lane == static_cast<uint32_t>(leader)) {
+      const uint32_t total = 8u * __popc(mask);
+      count_k<kSwz>(bins, overflow, mn, c_mn);
+      if (c_mn < total) count_k<kSwz>(bins, overflow, mx, total - c_mn);
+    }
     return;
   }
 #pragma unroll

@@ -351,7 +351,8 @@ def test_swizzled_and_flat_counter_wraps(gpu):
         assert D.read_stats(stats) == ref_st
 
 
-@pytest.mark.parametrize("variant", ["plain", "plain_swizzled", "few", "few_swizzled"])
+@pytest.mark.parametrize("variant", ["plain", "plain_swizzled", "few", "few_swizzled", "few_random",
+                                     "few_random_swizzled"])
 def test_counter_wraps_every_count_variant(gpu, variant):
     """Each of the four count-pass variants (smem layout plain / swizzled x
     repetitive-data probe off / on, picked per launch from a fixed sample)
@@ -361,8 +362,10 @@ def test_counter_wraps_every_count_variant(gpu, variant):
     base = np.array([0x3000, 0x3008] if "swizzled" in variant else [1000, 1001], dtype=np.uint16)
     if variant.startswith("plain"):
         vals = base[np.arange(n) % 2]               # adjacent samples always differ
+    elif "random" in variant:                        # binary noise: the min/max path
+        vals = base[np.random.default_rng(5).integers(0, 2, n)]
     else:
-        vals = base[(np.arange(n) // 37) % 2]       # runs of 37: repetitive
+        vals = base[(np.arange(n) // 37) % 2]       # runs of 37: flat + binary vectors
     img = torch.from_numpy(vals.view(np.int16)).to(gpu)
     hist = torch.zeros(65536, dtype=torch.int32, device=gpu)
     ws = D.lut_workspace(n)
