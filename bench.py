@@ -630,9 +630,17 @@ def c5_leg(n_gpus: int) -> dict:
             # requests in flight -- 3-6x slower than steady state
             # (tools/c5_probe.py), and not what a running server pays
             c5_run(srv.port, imgs, B, "bf16")
+            st0 = srv.stats()
             res = c5_run(srv.port, imgs, B, "bf16")
+            st1 = srv.stats()
     finally:
         G.init([0])
+    nreq = max(1, st1["requests"] - st0["requests"])
+    res["phases_ms_per_request"] = {
+        k: round((st1[k] - st0[k]) / nreq, 3) for k in ("recv_ms", "task_ms", "send_ms")}
+    res["phases_note"] = ("server-side, averaged over the timed pass's requests: payload "
+                          "received (TCP, H2D chunks overlapped) | task work after the last "
+                          "payload byte (kernels, D2H) | response written (TCP)")
     res.update({"workload": f"C5: {C5_REQUESTS} concurrent clients x (LUT_GEN -> LUT_APPLY -> "
                             f"MATMUL prec=bf16), {C5_IMG}^2 u16 images, {C5_MM}^3 matmul",
                 "server": "gpcx B200 server (max_tasks = 2 x hw threads), loopback TCP, "

@@ -295,6 +295,14 @@ int gpcx_server_start(const char* bind_addr, uint16_t port, int max_tasks,
                       int idle_timeout_ms, void** handle,
                       uint16_t* bound_port);
 int gpcx_server_stop(void* handle);
+/* Cumulative phase times of the requests a running server answered:
+ * payload received | remaining task work after the last payload byte |
+ * response written (milliseconds, summed over requests). */
+typedef struct gpcx_server_stats {
+  uint64_t requests;
+  double recv_ms, task_ms, send_ms;
+} gpcx_server_stats;
+int gpcx_server_stats_get(void* handle, gpcx_server_stats* out);
 /* Serve one request held in memory, like srv::handle_connection over a
  * wire::MemoryStream (server.cpp:51-112).  Writes the response frame bytes
  * to resp (resp_cap must hold it; *resp_len = bytes needed).  Returns the

@@ -16,7 +16,7 @@ import numpy as np
 
 from ._lib import (  # noqa: F401
     EXPORTS, PHASES, DeviceInfo, GpcxError, IMG_RAMP12, IMG_UNIFORM16, LIB_PATH, LUT_EQUALIZE,
-    LUT_STRETCH, LutStats, MAT_EXACT8, MAT_UNIFORM32, MODE_BY_NAME, PREC_BF16, PREC_BY_NAME,
+    LUT_STRETCH, LutStats, ServerStats, MAT_EXACT8, MAT_UNIFORM32, MODE_BY_NAME, PREC_BF16, PREC_BY_NAME,
     PREC_F32, PREC_TF32, STATUS, check, lib,
 )
 
@@ -164,6 +164,13 @@ class Server:
         if self._h.value:
             check(lib.gpcx_server_stop(self._h))
             self._h = C.c_void_p(None)
+
+    def stats(self) -> dict:
+        """Cumulative phase times (ms, summed) of the answered requests."""
+        st = ServerStats()
+        check(lib.gpcx_server_stats_get(self._h, C.byref(st)))
+        return {"requests": st.requests, "recv_ms": st.recv_ms, "task_ms": st.task_ms,
+                "send_ms": st.send_ms}
 
     def __enter__(self):
         return self.start()

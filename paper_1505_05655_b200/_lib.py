@@ -43,7 +43,7 @@ EXPORTS = [
     "gpcx_digest_u16_device", "gpcx_server_start", "gpcx_server_stop", "gpcx_handle_request",
     "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render", "gpcx_client_submit",
     "gpcx_lut_peer_create", "gpcx_lut_peer_ipc_handle", "gpcx_lut_peer_connect",
-    "gpcx_lut_peer_destroy", "gpcx_lut_correct_peer_device",
+    "gpcx_lut_peer_destroy", "gpcx_lut_correct_peer_device", "gpcx_server_stats_get",
 ]
 IPC_HANDLE_BYTES = 64
 
@@ -57,6 +57,11 @@ class DeviceInfo(C.Structure):
                 ("clock_rate_khz", C.c_int64), ("multi_processor_count", C.c_int32),
                 ("registers_per_block", C.c_int32), ("max_threads_per_block", C.c_int32),
                 ("max_grid_size", C.c_int32 * 3), ("max_threads_dim", C.c_int32 * 3)]
+
+
+class ServerStats(C.Structure):
+    _fields_ = [("requests", C.c_uint64), ("recv_ms", C.c_double), ("task_ms", C.c_double),
+                ("send_ms", C.c_double)]
 
 
 class LutStats(C.Structure):
@@ -124,6 +129,7 @@ def _load() -> C.CDLL:
         "gpcx_lut_peer_connect": ([vp, vp], i32),
         "gpcx_lut_peer_destroy": ([vp], i32),
         "gpcx_lut_correct_peer_device": ([vp, vp, vp, u64, i32, vp, vp, vp, u64, vp], i32),
+        "gpcx_server_stats_get": ([vp, vp], i32),
     }
     assert set(sig) == set(EXPORTS)
     for name, (args, res) in sig.items():

@@ -501,6 +501,15 @@ int gpcx_server_stop(void* handle) {
   });
 }
 
+int gpcx_server_stats_get(void* handle, gpcx_server_stats* out) {
+  return guarded([&] {
+    auto* h = static_cast<gpcx_server_handle*>(handle);
+    if (h == nullptr || out == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null argument");
+    const gpcx::srv::ServerStats st = h->server->stats();
+    *out = gpcx_server_stats{st.requests, st.recv_ms, st.task_ms, st.send_ms};
+  });
+}
+
 int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp, uint64_t resp_cap,
                         uint64_t* resp_len) {
   return guarded([&] {

@@ -298,3 +298,16 @@ def test_malformed_request_fuzz_over_tcp(server, refl):
                 assert ours == _raw_exchange(rs.port, req), (i, r["status"])
     status, _, _, _ = refl.ref_submit(server.port, "NOPE", "", b"", "a")
     assert status == "ERR:UNKNOWN_TASK"
+
+
+def test_server_phase_stats_count_answered_requests(refl):
+    """gpcx_server_stats_get: every answered request (here ERR frames, no
+    GPU needed) adds one request and non-negative phase times."""
+    with G.Server(max_tasks=2) as s:
+        assert s.stats()["requests"] == 0
+        for i in range(5):
+            status, _, _, _ = refl.ref_submit(s.port, "NOPE", f"i={i}", b"", "a")
+            assert status == "ERR:UNKNOWN_TASK"
+        st = s.stats()
+        assert st["requests"] == 5
+        assert all(st[k] >= 0.0 for k in ("recv_ms", "task_ms", "send_ms"))
