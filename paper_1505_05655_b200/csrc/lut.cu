@@ -78,18 +78,30 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 // Bank layout.  Values with trailing zero bits -- MSB-aligned 8 / 10 / 12
 // bit sensor data, multiples of 2^k -- put every lane of a warp on the same
 // bank (8-bit data x 128: 7.4 ms instead of 1.2 at 32768^2).  Such images
-// use the swizzled layout: word w at physical word swz(w), which XORs bits
-// 5-9 and 10-14 into the bank bits 0-4 (a bijection that only permutes the
-// words of each 32-word group, and its own inverse).  The LUT staged in
+// use a swizzled layout: word w at physical word swz1(w) / swz2(w), which
+// XOR bits 5-9 (and 10-14) into the bank bits 0-4 (bijections that only
+// permute the words of each 32-word group, each its own inverse).  The LUT staged in
 // smem for the apply pass uses the same layout.  The choice is made per
 // launch from a fixed sample of the image (`sample_layout`); it changes
 // only where counts live, never their values.
-__device__ __host__ __forceinline__ uint32_t swz(uint32_t w) {
+// Two strengths, picked from the sample's trailing zero count tz: tz 3-6
+// (12 / 10-bit data) XOR only bits 5-9 -- one instruction less per sample;
+// tz >= 7 (8-bit data) needs bits 10-14 as well (with bits 5-9 alone,
+// multiples of 256 still land on 8 banks: 1.82 vs 1.40 ms at 32768^2).
+__device__ __host__ __forceinline__ uint32_t swz1(uint32_t w) { return w ^ ((w >> 5) & 31u); }
+__device__ __host__ __forceinline__ uint32_t swz2(uint32_t w) {
   return w ^ (((w >> 5) ^ (w >> 10)) & 31u);
 }
-template <bool kSwz>
+// physical word of logical word w in layout kSwz (0 plain, 1, 2)
+template <int kSwz>
+__device__ __forceinline__ uint32_t phys_word(uint32_t w) {
+  if constexpr (kSwz == 1) return swz1(w);
+  else if constexpr (kSwz == 2) return swz2(w);
+  else return w;
+}
+template <int kSwz>
 __device__ __forceinline__ uint32_t word_of(uint32_t v) {
-  return kSwz ? swz(v >> 1) : (v >> 1);
+  return phys_word<kSwz>(v >> 1);
 }
 
 // Add k (<= 65535) samples of value v.  The thread whose atomic wraps a
@@ -97,7 +109,7 @@ __device__ __forceinline__ uint32_t word_of(uint32_t v) {
 // for a low-half carry into the high half, the spurious +1) into the global
 // overflow counters; the merge adds them back mod 2^32.  Exact for any
 // count < 2^32 and independent of the interleaving.
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void count_k(uint32_t* bins, uint32_t* overflow, uint32_t v,
                                         uint32_t k) {
   const uint32_t hi_bin = v & 1u;
@@ -113,7 +125,7 @@ __device__ __forceinline__ void count_k(uint32_t* bins, uint32_t* overflow, uint
   }
 }
 
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void count_one(uint32_t* bins, uint32_t* overflow, uint32_t v) {
   const uint32_t hi_bin = v & 1u;
   const uint32_t inc = hi_bin ? 0x10000u : 1u;
@@ -130,7 +142,7 @@ __device__ __forceinline__ void count_one(uint32_t* bins, uint32_t* overflow, ui
 // their (rare) wrap checks OR-ed into one branch per vector instead of a
 // branch (and its reconvergence pair) after each atomic -- C3 step 1.211 ->
 // 1.195 ms.
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
                                                 uint32_t* overflow, uint4 q) {
   const uint32_t v[8] = {q.x & 0xFFFFu, q.x >> 16, q.y & 0xFFFFu, q.y >> 16,
@@ -162,7 +174,7 @@ __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
 // few banks combines them first -- one or two atomics when the warp vector
 // holds at most two values (flat / binary: warp min, max and a count),
 // else one per distinct value per sample slot (__match_any_sync).
-template <bool kSwz>
+template <int kSwz>
 __device__ __noinline__ void count_vec_few(uint32_t* bins, uint32_t* overflow, uint4 q,
                                            uint32_t mask) {
   const uint32_t v[8] = {q.x & 0xFFFFu, q.x >> 16, q.y & 0xFFFFu, q.y >> 16,
@@ -212,12 +224,12 @@ __device__ __noinline__ void count_vec_few(uint32_t* bins, uint32_t* overflow, u
 }
 
 // Few distinct words among the warp's first samples of the vectors?
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ uint32_t bank_bit(uint4 q) {
   return 1u << (word_of<kSwz>(q.x & 0xFFFFu) & 31u);
 }
 
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void count_vec(uint32_t* bins, uint32_t* overflow, uint4 q) {
   const uint32_t mask = __activemask();
   if (__popc(__reduce_or_sync(mask, bank_bit<kSwz>(q))) <= 4) count_vec_few<kSwz>(bins, overflow, q, mask);
@@ -225,7 +237,7 @@ __device__ __forceinline__ void count_vec(uint32_t* bins, uint32_t* overflow, ui
 }
 
 // The main loop's two vectors share one probe (half its cost per sample).
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, uint4 q0,
                                            uint4 q1) {
   const uint32_t mask = __activemask();
@@ -240,9 +252,9 @@ __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, u
 
 // Per-launch choices from a fixed sample -- 256 pairs of adjacent samples
 // spread over the image, the same in every CTA:
-//   bit 0  swizzled layout: the OR of the samples has >= 3 trailing zero
-//          bits, i.e. the image looks MSB-aligned;
-//   bit 1  repetitive data: >= 1/8 of the pairs are equal (flat regions,
+//   bits 0-1  smem layout: 0 plain; 1 / 2 swizzled when the OR of the
+//          samples has 3-6 / >= 7 trailing zero bits (MSB-aligned data);
+//   bit 2  repetitive data: >= 1/8 of the pairs are equal (flat regions,
 //          binary or few-level images; noise-free ramps too) -> the count
 //          pass probes each warp's diversity and combines equal values.
 //          Ordinary images skip that probe (it costs ~2.5% on them).
@@ -274,8 +286,11 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
   }
   o = __reduce_or_sync(0xFFFFFFFFu, o);
   eq = __reduce_add_sync(0xFFFFFFFFu, eq);
-  if (threadIdx.x == 0)
-    *flags = ((n != 0 && (o & 7u) == 0) ? 1u : 0u) | (eq >= 32 ? 2u : 0u);
+  if (threadIdx.x == 0) {
+    const uint32_t tz = o == 0 ? 32u : static_cast<uint32_t>(__ffs(o) - 1);
+    const uint32_t layout = (n == 0 || tz < 3) ? 0u : (tz <= 6 ? 1u : 2u);
+    *flags = layout | (eq >= 32 ? 4u : 0u);
+  }
 }
 
 // Samples before the first 16-byte boundary (pointers are at least 2-byte
@@ -289,12 +304,12 @@ __device__ __host__ __forceinline__ std::uint64_t head_len(const void* p,
 
 // LUT entry v of the smem LUT (u16 entries, two per word; swizzled words
 // when kSwz -- see the bank layout note above).
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ uint32_t lut_at(const std::uint16_t* s_lut, uint32_t v) {
-  return kSwz ? s_lut[(swz(v >> 1) << 1) | (v & 1u)] : s_lut[v];
+  return kSwz ? s_lut[(phys_word<kSwz>(v >> 1) << 1) | (v & 1u)] : s_lut[v];
 }
 
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q) {
   uint4 r;
   r.x = lut_at<kSwz>(s_lut, q.x & 0xFFFFu) | (lut_at<kSwz>(s_lut, q.x >> 16) << 16);
@@ -305,12 +320,12 @@ __device__ __forceinline__ uint4 lookup_vec(const std::uint16_t* s_lut, uint4 q)
 }
 
 // Stage the global LUT (logical order) into smem in the kSwz layout.
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void stage_lut(uint4* smem, const std::uint16_t* lut_g) {
   if constexpr (kSwz) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(lut_g);
     uint32_t* dst = reinterpret_cast<uint32_t*>(smem);
-    for (int w = threadIdx.x; w < kWords; w += blockDim.x) dst[swz(w)] = __ldcg(src + w);
+    for (int w = threadIdx.x; w < kWords; w += blockDim.x) dst[phys_word<kSwz>(w)] = __ldcg(src + w);
   } else {
     const uint4* src = reinterpret_cast<const uint4*>(lut_g);
     for (int i = threadIdx.x; i < kBins / 8; i += blockDim.x) smem[i] = __ldcg(src + i);
@@ -320,7 +335,7 @@ __device__ __forceinline__ void stage_lut(uint4* smem, const std::uint16_t* lut_
 // Histogram of img[0, n) into the packed smem bins; CTA `cta` of `ctas`
 // (grid-stride over 128-bit vectors, two-vector software pipeline: the next
 // stage's loads are in flight while this stage's 16 samples are counted).
-template <bool kSwz, bool kFew>
+template <int kSwz, bool kFew>
 __device__ __forceinline__ void count_image(const std::uint16_t* img,
                                             std::uint64_t n, int cta, int ctas,
                                             uint32_t* bins, uint32_t* overflow) {
@@ -368,7 +383,7 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
 // out = LUT[in] over [0, n) with the LUT in smem; CTA `cta` of `ctas`.
 // Two vectors per stage, the next stage's loads in flight while this one is
 // looked up and stored (tools/apply_bench.cu: = cudaMemcpy D2D bandwidth).
-template <bool kSwz>
+template <int kSwz>
 __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const std::uint16_t* in,
                                             std::uint16_t* out, std::uint64_t n, int cta,
                                             int ctas) {
@@ -556,11 +571,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (count && static_cast<int>(blockIdx.x) < nparts) {
     for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    switch (s_swz & 3u) {
-      case 0: count_image<false, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 1: count_image<true, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 2: count_image<false, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      default: count_image<true, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+    switch (s_swz & 7u) {
+      case 0: count_image<0, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 1: count_image<1, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 2: count_image<2, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 4: count_image<0, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      case 5: count_image<1, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      default: count_image<2, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
     }
     __syncthreads();
     LUT_STAMP(1);
@@ -570,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(2);
   if (count) grid.sync();
   LUT_STAMP(3);
-  const bool swizzled = (s_swz & 1u) != 0;  // published by a barrier above (read only with img)
+  const uint32_t layout = s_swz & 3u;  // published by a barrier above (read only with img)
 
   // ---- phase 2: merge this CTA's 512-bin slice
   const bool slice_cta = static_cast<int>(blockIdx.x) < kSlices;
@@ -600,11 +617,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // red[group][bin], bin = 8 * quad + j of the slice -- logical bins:
       // in the swizzled layout the quad's physical words 4 quad .. +3 hold
       // logical words swz(.)
-      if (swizzled) {
+      if (layout != 0) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint32_t pw = blockIdx.x * 256u + quad * 4u + (j >> 1);
-          bins[group * 512 + 2 * (swz(pw) - blockIdx.x * 256u) + (j & 1)] = acc[j];
+          const uint32_t lw = layout == 1 ? swz1(pw) : swz2(pw);  // involutions
+          bins[group * 512 + 2 * (lw - blockIdx.x * 256u) + (j & 1)] = acc[j];
         }
       } else {
 #pragma unroll
@@ -748,16 +766,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(7);
 
   // ---- phase 4: apply
-  if (swizzled) stage_lut<true>(smem_u4, lut);
-  else stage_lut<false>(smem_u4, lut);
+  const auto* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
+  if (layout == 1) stage_lut<1>(smem_u4, lut);
+  else if (layout == 2) stage_lut<2>(smem_u4, lut);
+  else stage_lut<0>(smem_u4, lut);
   __syncthreads();
   LUT_STAMP(8);
-  if (swizzled)
-    apply_image<true>(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
-                      gridDim.x);
-  else
-    apply_image<false>(reinterpret_cast<const std::uint16_t*>(smem_u4), img, out, n, blockIdx.x,
-                       gridDim.x);
+  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x);
 #ifdef GPCX_LUT_TRACE
   __syncthreads();
 #endif
@@ -871,19 +888,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t s_swz;
   sample_layout(in, n, &s_swz);
   __syncthreads();
-  const bool swizzled = (s_swz & 1u) != 0;
-  if (swizzled) stage_lut<true>(smem_u4, lut_g);
-  else stage_lut<false>(smem_u4, lut_g);
+  const uint32_t layout = s_swz & 3u;
+  if (layout == 1) stage_lut<1>(smem_u4, lut_g);
+  else if (layout == 2) stage_lut<2>(smem_u4, lut_g);
+  else stage_lut<0>(smem_u4, lut_g);
   __syncthreads();
   const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
   if (!vector_ok) {  // mismatched alignment of in/out: scalar path
     const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
     for (std::uint64_t i = tid; i < n; i += static_cast<std::uint64_t>(gridDim.x) * kThreads)
-      out[i] = swizzled ? lut_at<true>(s_lut, in[i]) : lut_at<false>(s_lut, in[i]);
+      out[i] = layout == 1 ? lut_at<1>(s_lut, in[i])
+                           : (layout == 2 ? lut_at<2>(s_lut, in[i]) : lut_at<0>(s_lut, in[i]));
     return;
   }
-  if (swizzled) apply_image<true>(s_lut, in, out, n, blockIdx.x, gridDim.x);
-  else apply_image<false>(s_lut, in, out, n, blockIdx.x, gridDim.x);
+  if (layout == 1) apply_image<1>(s_lut, in, out, n, blockIdx.x, gridDim.x);
+  else if (layout == 2) apply_image<2>(s_lut, in, out, n, blockIdx.x, gridDim.x);
+  else apply_image<0>(s_lut, in, out, n, blockIdx.x, gridDim.x);
 }
 
 bool g_attrs_set[64] = {};

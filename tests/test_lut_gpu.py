@@ -359,7 +359,10 @@ def test_counter_wraps_every_count_variant(gpu, variant):
     with > 65535 samples of a value per CTA, so the packed u16 halves wrap."""
     torch, D = _dev()
     n = 24_000_007  # 2 values over 148 CTAs: ~81K samples of each per CTA
-    base = np.array([0x3000, 0x3008] if "swizzled" in variant else [1000, 1001], dtype=np.uint16)
+    # swizzle strength from the trailing zeros: 0x3008 -> 3 (layout 1),
+    # 0x3100 -> 8 (layout 2)
+    base = np.array([0x3000, 0x3100] if variant == "few_random_swizzled" else
+                    [0x3000, 0x3008] if "swizzled" in variant else [1000, 1001], dtype=np.uint16)
     if variant.startswith("plain"):
         vals = base[np.arange(n) % 2]               # adjacent samples always differ
     elif "random" in variant:                        # binary noise: the min/max path

@@ -15,11 +15,17 @@ imgs = {
     "constant": lambda: torch.full((n,), 1234, dtype=torch.int16, device="cuda"),
     "two_values": lambda: (torch.randint(0, 2, (n,), device="cuda", generator=g, dtype=torch.int16) * 3000 + 100),
     "8bit_scaled": lambda: (torch.randint(0, 256, (n,), device="cuda", generator=g, dtype=torch.int16) * 128),
+    "msb12_x16": lambda: (torch.randint(0, 4096, (n,), device="cuda", generator=g, dtype=torch.int16) * 16),
+    "msb10_x64": lambda: (torch.randint(0, 1024, (n,), device="cuda", generator=g, dtype=torch.int16) * 64),
+    "msb8_x256": lambda: (torch.randint(0, 256, (n,), device="cuda", generator=g, dtype=torch.int32) * 256).to(torch.int16),
     "half_flat": lambda: torch.where(torch.arange(n, device="cuda") < n // 2, torch.tensor(500, dtype=torch.int16, device="cuda"),
                                      D.synth_image(0, 0x5EED, 32768, 32768)),
 }
 res = {}
+only = sys.argv[1:]
 for name, make in imgs.items():
+    if only and name not in only:
+        continue
     img = make()
     ts = []
     for i in range(6):
