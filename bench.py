@@ -5,14 +5,18 @@ host-CPU reference path.
 Primary line (BASELINE.json metric): LUT image correction (LUT_GEN equalize +
 LUT_APPLY, i.e. LUT_CORRECT) of the config-C3 scene, 32768 x 32768 u16
 (ramp12 synthetic), row-band sharded over N GPUs: each rank histograms its
-band, the 65536-bin histograms are all-reduced over NCCL (the one exchange
-step the equalize LUT needs), every rank builds the identical LUT and
-applies it to its band.  One step = one full LUT_CORRECT of the scene.
-The matmul figure (config C2, FP32 4096^3 through the SIMT kernel, and the
-tensor-core path once built) rides along in the "matmul" object.
+band, the 65536-bin histograms are summed (the one exchange step the
+equalize LUT needs: inside the kernel over peer memory by default, NCCL as
+the fallback), every rank builds the identical LUT and applies it to its
+band.  One step = one full LUT_CORRECT of the scene.  Riding along in the
+same JSON line: `stretch` (C3, mode=stretch), `demosaic` (§8f row 1),
+`matmul` (C4 bf16 32768^3 + its tf32 variant, C2 f32 4096^3), `e2e`, `c5`
+(64 chained requests through the server, with a phase breakdown), `c1`
+(one request over TCP and through the C ABI) and the CPU baselines.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+  python bench.py --gpc-bench --task T [--dims ...] [--workers-list ...]
 
 Timing: CUDA events on the stream the kernels are launched on, barrier +
 synchronize on both sides of the K timed steps, max over ranks.  Inputs are
