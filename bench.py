@@ -135,6 +135,11 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         if want != self.world and self.world != 1:
             raise SystemExit(f"--gpus {want} but WORLD_SIZE={self.world}")
+        if want > 1 and self.world == 1 and os.environ.get("GPCX_BENCH_SINGLE_PROCESS") != "1":
+            # one process would time only its own band while `value` counts
+            # the whole scene -- N > 1 is one process per GPU
+            raise SystemExit(f"--gpus {want} needs one process per GPU: "
+                             f"torchrun --nproc-per-node {want} bench.py --gpus {want}")
         self.n = want if self.world == 1 else self.world
         self.pg = None
 
