@@ -140,6 +140,10 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
   __shared__ __align__(16) std::uint16_t tile[TR + 2][SW];
   const int r0 = row_base + blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int row_end = row_base + out_rows;
+  // last image row staged for this band: its halo row below (row_end) or
+  // the image's last row -- a band's last tile may reach past its rows,
+  // whose outputs are skipped, and must not read past the band's buffer
+  const int last_row = min(rows - 1, row_end);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
       for (int j = 0; j < kBatch; ++j) {
         const int i = warp + (j0 + j) * (THREADS / 32);
         if (j0 + j < kRowsPerWarp && i < TR + 2) {
-          const int gr = min(max(r0 - 1 + i, 0), rows - 1);
+          const int gr = min(max(r0 - 1 + i, 0), last_row);
           const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr - in_row0) * cols;
           q[j] = __ldg(reinterpret_cast<const uint4*>(grow + c0) + lane);
           if (lane < 2) halo[j] = __ldg(grow + (lane == 0 ? max(c0 - 1, 0) : min(c0 + TC, cols - 1)));
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(THREADS, kMinBlocks<RPT>)
     }
   } else {
     for (int i = warp; i < TR + 2; i += THREADS / 32) {
-      const int gr = min(max(r0 - 1 + i, 0), rows - 1);
+      const int gr = min(max(r0 - 1 + i, 0), last_row);
       const std::uint16_t* grow = in + static_cast<std::uint64_t>(gr - in_row0) * cols;
       std::uint16_t* srow = tile[i];
       for (int c = lane; c < TC; c += 32) srow[kPad + c] = grow[min(c0 + c, cols - 1)];
