@@ -936,8 +936,8 @@ def run_b200(args) -> None:
         "workload": "C3 with mode=stretch (LUT from the global min/max)",
         "value": round(px_total * args.steps / (stretch_ms / 1e3) / 1e9, 2), "unit": "Gpixel/s",
         "ms_per_step": round(stretch_ms / args.steps, 4),
-        "kernels": ("lut::minmax_kernel (2 B/px, redux.sync min/max) + from_minmax + apply_kernel "
-                    "(4 B/px)" if d.n == 1 else "fused_kernel with the peer exchange, as equalize"),
+        "kernels": ("lut::stretch_fused_kernel, one cooperative launch: min/max (2 B/px, redux.sync) "
+                    "| grid sync | per-CTA stretch LUT in smem | apply (4 B/px)" if d.n == 1 else "fused_kernel with the peer exchange, as equalize"),
         "roofline": {"bound": "hbm", "achieved": round(st_ach, 1), "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": round(st_ach / pk["hbm_gbs"], 4),
                      "algorithmic_bytes_per_step": 6 * band_px},

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cuda_util.hpp"
 #include "kernels.hpp"
@@ -906,6 +907,107 @@ __global__ void __launch_bounds__(kThreads, 1)
   else apply_image<0>(s_lut, in, out, n, blockIdx.x, gridDim.x);
 }
 
+// LUT_CORRECT stretch in ONE cooperative launch (1 CTA x 1024 threads per
+// SM) instead of min/max + reduce + LUT + apply: per-CTA min/max of the
+// image -> grid sync -> every CTA reduces the slots and builds the whole
+// stretch LUT straight into its own smem (64 entries per thread, no second
+// grid-wide step; CTA b also stores 1024-word slices b, b + grid, ... of
+// the caller's LUT, CTA 0 the stats) -> apply.  Same entries as
+// from_minmax_kernel (stretch_entry), so bit-identical.
+template <int kSwz>
+__device__ __forceinline__ void build_stretch_lut(uint32_t* s_words, std::uint16_t* lut_g,
+                                                  std::uint64_t n, std::uint64_t lo,
+                                                  std::uint64_t hi) {
+#pragma unroll 4
+  for (int k = 0; k < kWords / kThreads; ++k) {
+    const uint32_t w = static_cast<uint32_t>(k * kThreads) + threadIdx.x;
+    const uint32_t e = stretch_entry(2 * w, n, lo, hi) | (stretch_entry(2 * w + 1, n, lo, hi) << 16);
+    s_words[phys_word<kSwz>(w)] = e;
+    if (k % static_cast<int>(gridDim.x) == static_cast<int>(blockIdx.x))
+      reinterpret_cast<uint32_t*>(lut_g)[w] = e;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    stretch_fused_kernel(const std::uint16_t* img, std::uint16_t* out,  // may alias (in place)
+                         std::uint64_t n, uint2* __restrict__ slots, std::uint16_t* lut_g,
+                         gpcx_lut_stats* stats) {
+  extern __shared__ uint4 smem_u4[];
+  __shared__ uint32_t smn[32], smx[32], s_swz;
+  cg::grid_group grid = cg::this_grid();
+  sample_layout(img, n, &s_swz);
+  uint32_t mn2 = 0xFFFFFFFFu, mx2 = 0;
+  {
+    const std::uint64_t head = head_len(img, n);
+    const std::uint64_t nvec = (n - head) >> 3;
+    const std::uint64_t tail0 = head + (nvec << 3);
+    const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kThreads;
+    if (tid < head) {
+      const uint32_t v = img[tid];
+      mn2 = __vminu2(mn2, v | (v << 16));
+      mx2 = __vmaxu2(mx2, v | (v << 16));
+    }
+    if (tid < n - tail0) {
+      const uint32_t v = img[tail0 + tid];
+      mn2 = __vminu2(mn2, v | (v << 16));
+      mx2 = __vmaxu2(mx2, v | (v << 16));
+    }
+    const uint4* body = reinterpret_cast<const uint4*>(img + head);
+    std::uint64_t i = tid;
+    for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+      uint4 q[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) q[u] = ld_stream(body + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) minmax_vec(q[u], mn2, mx2);
+    }
+    for (; i < nvec; i += stride) minmax_vec(ld_stream(body + i), mn2, mx2);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, min(mn2 & 0xFFFFu, mn2 >> 16));
+  uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, max(mx2 & 0xFFFFu, mx2 >> 16));
+  if (lane == 0) {
+    smn[warp] = mn;
+    smx[warp] = mx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    mn = __reduce_min_sync(0xFFFFFFFFu, smn[lane]);
+    mx = __reduce_max_sync(0xFFFFFFFFu, smx[lane]);
+    if (lane == 0) slots[blockIdx.x] = make_uint2(mn, mx);
+  }
+  grid.sync();
+  if (warp == 0) {
+    mn = 0xFFFFFFFFu;
+    mx = 0;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+      const uint2 sl = __ldcg(slots + b);
+      mn = min(mn, sl.x);
+      mx = max(mx, sl.y);
+    }
+    mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+    mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+    if (lane == 0) {
+      smn[0] = mn;
+      smx[0] = mx;
+      if (blockIdx.x == 0) *stats = gpcx_lut_stats{n, mn, mx, 0};
+    }
+  }
+  __syncthreads();
+  const std::uint64_t lo = smn[0], hi = smx[0];
+  const uint32_t layout = s_swz & 3u;
+  uint32_t* s_words = reinterpret_cast<uint32_t*>(smem_u4);
+  if (layout == 1) build_stretch_lut<1>(s_words, lut_g, n, lo, hi);
+  else if (layout == 2) build_stretch_lut<2>(s_words, lut_g, n, lo, hi);
+  else build_stretch_lut<0>(s_words, lut_g, n, lo, hi);
+  __syncthreads();
+  const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
+  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+}
+
 bool g_attrs_set[64] = {};
 
 void set_attrs_once() {
@@ -915,6 +1017,8 @@ void set_attrs_once() {
   GPCX_CUDA(cudaFuncSetAttribute(fused_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemHist));
   GPCX_CUDA(cudaFuncSetAttribute(apply_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLut));
+  GPCX_CUDA(cudaFuncSetAttribute(stretch_fused_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLut));
   if (dev < 64) g_attrs_set[dev] = true;
 }
@@ -959,6 +1063,15 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
                                         kSmemHist, stream));
 }
 
+// GPCX_LUT_STRETCH_FUSED=0: the four-launch stretch path (A/B only).
+bool stretch_fused_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("GPCX_LUT_STRETCH_FUSED");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
+}
+
 bool co_aligned(const void* a, const void* b) {
   return ((reinterpret_cast<std::uintptr_t>(a) ^ reinterpret_cast<std::uintptr_t>(b)) & 15u) == 0;
 }
@@ -996,6 +1109,15 @@ void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n
                     std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
   if (mode == GPCX_LUT_EQUALIZE && co_aligned(in, out) && n != 0) {
     launch_fused(kCount | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream);
+    return;
+  }
+  if (mode == GPCX_LUT_STRETCH && co_aligned(in, out) && n != 0 && stretch_fused_enabled()) {
+    set_attrs_once();
+    auto* slots = reinterpret_cast<uint2*>(static_cast<unsigned char*>(ws) + kMinMaxOff);
+    const int sms = device_sm_count();
+    void* args[] = {const_cast<std::uint16_t**>(&in), &out, &n, &slots, &lut, &stats};
+    GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(stretch_fused_kernel),
+                                          dim3(sms), dim3(kThreads), args, kSmemLut, stream));
     return;
   }
   if (mode == GPCX_LUT_EQUALIZE) {

@@ -118,23 +118,25 @@ def test_apply_unaligned_and_inplace(gpu, in_off, out_off):
     assert np.array_equal(u16(inplace), lut_np[u16(src)])
 
 
+@pytest.mark.parametrize("mode", [O.LUT_EQUALIZE, O.LUT_STRETCH])
 @pytest.mark.parametrize("in_off,out_off", [(0, 0), (1, 1), (3, 3), (1, 0), (0, 5), (None, None)])
-def test_lut_correct_fused_alignment_and_inplace(gpu, in_off, out_off):
-    """LUT_CORRECT equalize is one cooperative launch when in/out are
-    co-aligned (incl. in place), the gen + apply pair otherwise: same bytes."""
+def test_lut_correct_fused_alignment_and_inplace(gpu, in_off, out_off, mode):
+    """LUT_CORRECT (equalize: fused_kernel, stretch: stretch_fused_kernel) is
+    one cooperative launch when in/out are co-aligned (incl. in place), the
+    gen + apply launches otherwise: same bytes."""
     torch, D = _dev()
     n = 1_000_003
     base = D.synth_image(O.IMG_RAMP12, 9, 1, n + 16)
     if in_off is None:  # in place
         src = base[3:3 + n].clone()
-        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), O.LUT_EQUALIZE)
+        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), mode)
         dst = src
     else:
         src = base[in_off:in_off + n]
-        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), O.LUT_EQUALIZE)
+        ref_out, ref_lut, ref_st = O.lut_correct(u16(src), mode)
         dst = torch.zeros(n + 16, dtype=torch.int16, device=gpu)[out_off:out_off + n]
     lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
-    D.lut_correct(src, dst, O.LUT_EQUALIZE, lut, stats, ws)
+    D.lut_correct(src, dst, mode, lut, stats, ws)
     assert np.array_equal(u16(dst), ref_out)
     assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
 
