@@ -11,7 +11,11 @@
 //                   selected per call: histogram (1 CTA/SM, 128 KiB smem of
 //                   packed u16 pairs, 128-bit streaming loads, 2 B/px) ->
 //                   partial merge -> LUT -> apply (4 B/px).
-//   minmax_kernel   warp-shuffle (redux) min/max for stretch.  2 B/px read.
+//   stretch_fused_kernel  LUT_CORRECT stretch, one cooperative launch:
+//                   min/max (2 B/px) -> grid sync -> per-CTA LUT in smem ->
+//                   apply (4 B/px).
+//   minmax_kernel   warp-shuffle (redux) min/max for LUT_GEN stretch and
+//                   non-co-aligned LUT_CORRECT stretch.  2 B/px read.
 //   from_minmax     stretch LUT.
 //   apply_kernel    LUT_APPLY: persistent, LUT staged in 128 KiB smem,
 //                   128-bit loads/stores, 8 gathers per vector.   4 B/px.
