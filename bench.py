@@ -174,6 +174,14 @@ class Dist:
             self.pg.all_reduce(h)
             t.copy_(h)
 
+    def sum_u64(self, x: int) -> int:
+        """Sum of a Python int over ranks, mod 2^64 (band digests)."""
+        if self.pg is None:
+            return x
+        xs = [None] * self.n
+        self.pg.all_gather_object(xs, x)
+        return sum(xs) & (2 ** 64 - 1)
+
     def barrier(self):
         if self.pg is not None:
             self.pg.barrier()
@@ -312,7 +320,10 @@ def lut_device_leg(d: Dist, steps: int, warmup: int, mode: int, gather: bool = T
                if ev["a0"] else None)
     # correctness guard on the measured buffers (device digest vs nothing
     # here; the oracle check of this exact band runs in the cpu leg).
+    # parity of the timed output: the band's position-keyed digest (additive
+    # over bands), summed over ranks and compared with the oracle's by rank 0
     dig = int(D.digest_u16(out, r0 * COLS).item()) & (2 ** 64 - 1)
+    dig = d.sum_u64(dig)
     st = D.read_stats(stats)
     gather_ms = gather_leg(d, out) if d.pg is not None and gather else None
     if peer is not None:
@@ -759,21 +770,53 @@ def cpu_c1() -> dict:
     return res
 
 
-def cpu_lut(mode: int, sample_rows: int = 4096, reps: int = 3) -> dict:
-    """The restated oracle (kind "port") on a row-band sample of the C3
-    scene with every host thread; returns Gpx/s and the band digest."""
+def c3_config(n: int) -> dict:
+    """The C3 workload as both arms name it (`same_config`)."""
+    return {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene, row bands",
+            "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
+            "parallelism": f"row-band x{n}", "l2": "inputs larger than L2 (2 GiB scene)"}
+
+
+def cpu_lut_full(modes=(0, 1), reps: int = 3, threads: int = 0) -> dict:
+    """The restated oracle (kind "port"; the reference has no LUT code) on
+    the WHOLE C3 scene with every host thread: per mode the median
+    LUT_CORRECT time over `reps` runs, the output's position-keyed digest
+    and the stats -- the CPU baseline and the parity reference of the timed
+    GPU output at once."""
     from oracle import oracle as O
-    img = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS, 0, sample_rows)
-    times = []
-    for _ in range(reps):
-        t = time.perf_counter()
-        O.lut_correct(img, mode)
-        times.append(time.perf_counter() - t)
-    px = sample_rows * COLS
-    return {"value": px / statistics.median(times) / 1e9, "unit": "Gpixel/s",
-            "cores": O.max_threads(), "kind": "port",
-            "sample": f"LUT_CORRECT equalize on a {sample_rows}x{COLS} band of the C3 scene, "
-                      f"median of {reps}, oracle/gpcx_oracle.c with {O.max_threads()} OpenMP threads",
+    threads = threads or O.max_threads()
+    scene = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS)
+    res = {}
+    for mode in modes:
+        times = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            out, _, st = O.lut_correct(scene, mode, threads=threads)
+            times.append(time.perf_counter() - t)
+        res[mode] = {"s": statistics.median(times), "digest": O.digest_u16(out), "stats": st,
+                     "reps": reps}
+        del out
+    res["cores"] = threads
+    return res
+
+
+def lut_parity(leg: dict, ref: dict) -> dict:
+    """Timed GPU output vs the oracle on the same scene: bit-exact through
+    the position-keyed u64 digest (sum over all 2^30 pixels) and the stats."""
+    ok = leg["digest"] == ref["digest"] and leg["stats"] == ref["stats"]
+    return {"ok": bool(ok), "digest": f"{leg['digest']:016x}", "oracle_digest": f"{ref['digest']:016x}",
+            "stats": leg["stats"], "how": "sum_i splitmix64(i ^ out[i]) mod 2^64 over the whole "
+                                          "timed output vs oracle/gpcx_oracle.c LUT_CORRECT of the scene"}
+
+
+def cpu_lut(ref: dict, mode: int) -> dict:
+    from oracle import oracle as O
+    r = ref[mode]
+    return {"value": ROWS * COLS / r["s"] / 1e9, "unit": "Gpixel/s", "cores": ref["cores"],
+            "kind": "port",
+            "sample": f"LUT_CORRECT {'equalize' if mode == 0 else 'stretch'} of the whole {ROWS}x{COLS} "
+                      f"C3 scene (no sampling), median of {r['reps']}, oracle/gpcx_oracle.c with "
+                      f"{ref['cores']} OpenMP threads",
             "host": O.host_cpu()}
 
 
@@ -918,13 +961,11 @@ def run_b200(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic (ramp12 splitmix64 scene, generated on device)",
-            "config": {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene, row bands",
-                       "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12",
-                       "parallelism": (f"row-band x{d.n}" if d.n == 1 else
-                                       f"row-band x{d.n}, 65536-bin histogram exchange: "
-                                       + ("fused into the kernel over peer memory (IPC / NVLink P2P)"
-                                          if lut["exchange"] == "peer" else "NCCL all-reduce")),
-                       "l2": "inputs larger than L2 (2 GiB scene)"},
+            "config": c3_config(d.n),
+            "exchange": (None if d.n == 1 else
+                         "65536-bin histogram exchange " + ("fused into the kernel over peer memory "
+                                                            "(IPC / NVLink P2P)" if lut["exchange"] == "peer"
+                                                            else "by NCCL all-reduce")),
             # per step: fused_kernel once (N=1, or N>1 with the peer exchange);
             # count + build/apply launches with the NCCL exchange
             "roofline": roof, "gpu_launches": launches * args.steps,
@@ -1028,8 +1069,15 @@ def run_b200(args) -> None:
         line["demosaic"]["e2e"] = demosaic_task_leg()
     # CPU baselines last: their all-core OpenMP runs heat the host and slow
     # the TCP-bound C5 leg if they run before it
+    # parity of the timed outputs (equalize and stretch) against the oracle
+    # on the whole scene; at N=1 the same oracle runs are the CPU baseline
+    ref = cpu_lut_full(reps=3 if d.n == 1 else 1)
+    line["parity"] = {"equalize": lut_parity(lut, ref[0]), "stretch": lut_parity(stretch, ref[1])}
+    line["parity"]["ok"] = line["parity"]["equalize"]["ok"] and line["parity"]["stretch"]["ok"]
+    line["stretch"]["parity"] = line["parity"]["stretch"]["ok"]
     if d.n == 1:
-        line["cpu_baseline"] = cpu_lut(mode)
+        line["cpu_baseline"] = cpu_lut(ref, mode)
+        line["stretch"]["cpu_baseline"] = cpu_lut(ref, 1)
         if mm is not None:
             line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
         if dm is not None:
@@ -1051,8 +1099,10 @@ def run_b200(args) -> None:
 
 
 def run_reference(args) -> None:
-    """The reference arm: the restated CPU path on the host cores (there is
-    no reference LUT / matmul implementation to install)."""
+    """The reference arm: the restated CPU path (oracle/gpcx_oracle.c; the
+    reference has no LUT / matmul implementation to install, SURVEY.md
+    §0.3) on the box's host cores, on the SAME workload as the B200 arm --
+    LUT_CORRECT equalize of the whole 32768^2 C3 scene per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -1062,24 +1112,24 @@ def run_reference(args) -> None:
     os.environ["OMP_NUM_THREADS"] = str(cores)
     from oracle import oracle as O
     mode = 0
-    sample_rows = 2048
-    img = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS, 0, sample_rows)
+    img = O.synth_image(O.IMG_RAMP12, SEED, ROWS, COLS)
     times = []
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
-        O.lut_correct(img, mode, threads=cores)
+        out, _, st = O.lut_correct(img, mode, threads=cores)
         if i >= args.warmup:
             times.append(time.perf_counter() - t)
-    px = sample_rows * COLS
+    dig = O.digest_u16(out)
+    px = ROWS * COLS
     value = px * len(times) / sum(times) / 1e9
-    sample = (f"LUT_CORRECT equalize on a {sample_rows}x{COLS} band of the C3 scene per step, "
-              f"oracle/gpcx_oracle.c (restatement; the reference has no LUT code)")
+    sample = (f"LUT_CORRECT equalize of the whole {ROWS}x{COLS} C3 scene per step (no sampling), "
+              f"oracle/gpcx_oracle.c (restatement; the reference has no LUT code), {cores} OpenMP threads")
     line = {"metric": METRIC, "value": round(value, 4), "unit": "Gpixel/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-            "config": {"workload": "C3: LUT_CORRECT equalize, 32768x32768 u16 scene (sampled band)",
-                       "rows": ROWS, "cols": COLS, "mode": "equalize", "image": "ramp12"},
+            "config": c3_config(args.gpus),
+            "output": {"digest": f"{dig:016x}", "stats": st},
             "cpu_baseline": {"value": round(value, 4), "unit": "Gpixel/s", "cores": cores,
                              "kind": "port", "sample": sample, "host": O.host_cpu()},
             "e2e": {"value": round(value, 4), "unit": "Gpixel/s", "h2d_bytes_per_step": 0,

@@ -220,7 +220,13 @@ int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n,
  *      (system-scope flags), sum their histograms with P2P loads, build the
  *      identical LUT on every rank, apply it to the band.
  * A rank whose peers never arrive traps after GPCX_PEER_TIMEOUT_MS (default
- * 60000) and the call's stream reports the failure. */
+ * 60000) and the call's stream reports the failure.
+ * Sizes: each rank's band n < 2^32 (its own histogram is u32); the group's
+ * summed histogram, its totals, cdf_min and stats.n are 64-bit, so the whole
+ * image may hold up to nranks * (2^32 - 1) pixels (8 ranks: ~2^35, e.g. a
+ * 131072 x 262143 scene).  (gpcx_lut_correct_from_hist_device takes a u32
+ * histogram: a caller that all-reduces band histograms itself must keep the
+ * image below 2^32 pixels or pass per-bin sums that fit in u32.) */
 #define GPCX_IPC_HANDLE_BYTES 64
 typedef struct gpcx_lut_peer gpcx_lut_peer;
 int gpcx_lut_peer_create(int rank, int nranks, gpcx_lut_peer** out);

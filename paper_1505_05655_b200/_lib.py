@@ -7,6 +7,7 @@ usable, every compute call fails with GPCX_E_TASK_FAILED (-> GpcxError).
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgpcx.so"
@@ -77,7 +78,18 @@ class GpcxError(RuntimeError):
         super().__init__(f"{self.code}: {message}")
 
 
+def _building() -> bool:
+    """`python -m paper_1505_05655_b200.build`: Python imports this package
+    (and so this module) before it runs build.py, so a clean checkout must
+    not fail here -- the library is built first, then loaded."""
+    argv = list(getattr(sys, "orig_argv", []))
+    return "-m" in argv and argv[argv.index("-m") + 1:argv.index("-m") + 2] == [f"{__package__}.build"]
+
+
 def _load() -> C.CDLL:
+    if not LIB_PATH.exists() and _building():
+        import runpy
+        runpy.run_path(str(LIB_PATH.parent.parent / "build.py"), run_name="build_only")["build"]()
     if not LIB_PATH.exists():
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python paper_1505_05655_b200/build.py` "

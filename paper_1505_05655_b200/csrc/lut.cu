@@ -426,10 +426,13 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
   for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec<kSwz>(s_lut, ld_stream(src + i)));
 }
 
-// floor(num / d) for num < 2^50 and d >= 1 without a 64-bit integer divide
-// (a ~70-instruction software sequence): the f64 estimate num * (1/d) is
-// within 1/8 of the true quotient, so truncation is off by at most one and a
-// single remainder test fixes it.  Bit-exact with the oracle's integer '/'.
+// floor(num / d) for num < 2^53 and d >= 1 without a 64-bit integer divide
+// (a ~70-instruction software sequence): num converts to f64 exactly and
+// num * (1/d) carries a relative error of ~2^-52, so for the quotients here
+// (<= 65535) the estimate is far within 1 of the true quotient; truncation
+// is off by at most one and a single remainder test fixes it.  Bit-exact with
+// the oracle's integer '/'.  Largest use: an 8-rank group of 2^32-1-sample
+// bands, num < 2^35 * 65536 = 2^51.
 __device__ __forceinline__ std::uint64_t udiv_exact(std::uint64_t num, std::uint64_t d,
                                                     double inv_d) {
   std::uint64_t q = static_cast<std::uint64_t>(static_cast<double>(num) * inv_d);
@@ -553,16 +556,32 @@ __device__ void peer_rendezvous(const PeerTable* P, int slice, std::uint32_t seq
   }
 }
 
+// Phase 2 -> phase 3 summary of one 512-bin slice.  Totals are 64-bit: one
+// call's band is < 2^32 samples (its histogram is u32), but the histogram
+// summed over a group of ranks can reach kMaxRanks * (2^32 - 1).
+struct SliceSummary {
+  unsigned long long total, first_count;  // sum of the slice's bins, count of `first`
+  uint32_t first, last, pad0, pad1;       // first / last non-empty bin (0xFFFFFFFF / 0 if none)
+};
+static_assert(sizeof(SliceSummary) * kSlices <= kPartsOff - kBlocksOff, "summaries fit the workspace");
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+#pragma unroll
+  for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, d);
+  return x;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int nparts,
                  uint32_t* __restrict__ parts, uint32_t* __restrict__ overflow,
-                 uint32_t* __restrict__ hist, uint4* __restrict__ blocks, int mode,
+                 uint32_t* __restrict__ hist, SliceSummary* __restrict__ blocks, int mode,
                  std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
                  int stages, const PeerTable* __restrict__ peers, std::uint32_t seq,
                  unsigned long long timeout_ns) {
   extern __shared__ uint4 smem_u4[];
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
-  __shared__ uint32_t s_wsum[8], s_wfirst[8], s_wlast[8], s_wfcount[8];
+  __shared__ unsigned long long s_wsum[8], s_wfcount[8];
+  __shared__ uint32_t s_wfirst[8], s_wlast[8];
   cg::grid_group grid = cg::this_grid();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
@@ -597,7 +616,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- phase 2: merge this CTA's 512-bin slice
   const bool slice_cta = static_cast<int>(blockIdx.x) < kSlices;
   const int w = blockIdx.x * 256 + t;  // word (bins 2w, 2w+1) of threads t < 256
-  uint32_t c0 = 0, c1 = 0, inc = 0;
+  // bins 2w, 2w+1 of the (group's) histogram: u64 once peers are summed in
+  unsigned long long c0 = 0, c1 = 0, inc = 0;
   if (slice_cta) {
     if (count) {
       const int quad = t & 63, group = t >> 6;
@@ -648,7 +668,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<uint2*>(overflow)[w] = make_uint2(0, 0);
         c0 = lo + ov.x;
         c1 = hi + ov.y;
-        reinterpret_cast<uint2*>(hist)[w] = make_uint2(c0, c1);
+        // this band's own histogram (< 2^32 samples per call: exact in u32)
+        reinterpret_cast<uint2*>(hist)[w] = make_uint2(static_cast<uint32_t>(c0),
+                                                       static_cast<uint32_t>(c1));
       } else if (!exchange) {
         const uint2 h = __ldcg(reinterpret_cast<const uint2*>(hist) + w);
         c0 = h.x;
@@ -678,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       inc = c0 + c1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
         if (lane >= d) inc += y;
       }
       const uint32_t first = c0 ? 2u * w : (c1 ? 2u * w + 1 : 0xFFFFFFFFu);
@@ -686,8 +708,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t wfirst = __reduce_min_sync(0xFFFFFFFFu, first);
       const uint32_t wlast = __reduce_max_sync(0xFFFFFFFFu, last);
       // count of the first non-empty bin (cdf_min if it is the global one)
-      const uint32_t wfcount = __reduce_add_sync(
-          0xFFFFFFFFu, first == wfirst && first != 0xFFFFFFFFu ? (c0 ? c0 : c1) : 0u);
+      const unsigned long long wfcount =
+          warp_sum_u64(first == wfirst && first != 0xFFFFFFFFu ? (c0 ? c0 : c1) : 0ull);
       if (lane == 31) s_wsum[warp] = inc;
       if (lane == 0) {
         s_wfirst[warp] = wfirst;
@@ -697,7 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     if (t == 0) {
-      uint32_t sum = 0, first = 0xFFFFFFFFu, last = 0, fcount = 0;
+      unsigned long long sum = 0, fcount = 0;
+      uint32_t first = 0xFFFFFFFFu, last = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         sum += s_wsum[i];
@@ -708,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         last = max(last, s_wlast[i]);
       }
       // (total, first, last, count(first)): phase 3 needs no second load
-      blocks[blockIdx.x] = make_uint4(sum, first, last, fcount);
+      blocks[blockIdx.x] = SliceSummary{sum, fcount, first, last, 0u, 0u};
     }
   }
   LUT_STAMP(4);
@@ -718,27 +741,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- phase 3: LUT slice
   if (slice_cta && t < 256) {
-    uint32_t n32 = 0, off = 0, lo = 0xFFFFFFFFu, hi = 0, lo_count = 0;
+    unsigned long long n64 = 0, off = 0, lo_count = 0;
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
     static_assert(kSlices % 32 == 0, "whole warps of slice triples");
 #pragma unroll
     for (int b0 = 0; b0 < kSlices; b0 += 32) {
       const int b = b0 + lane;
-      const uint4 q = __ldcg(blocks + b);
-      n32 += q.x;
-      if (b < static_cast<int>(blockIdx.x)) off += q.x;
-      if (q.y < lo) {  // slices are disjoint: each first bin is distinct
-        lo = q.y;
-        lo_count = q.w;
+      const ulonglong2 tc = __ldcg(reinterpret_cast<const ulonglong2*>(blocks + b));
+      const uint2 fl = __ldcg(reinterpret_cast<const uint2*>(blocks + b) + 2);
+      n64 += tc.x;
+      if (b < static_cast<int>(blockIdx.x)) off += tc.x;
+      if (fl.x < lo) {  // slices are disjoint: each first bin is distinct
+        lo = fl.x;
+        lo_count = tc.y;
       }
-      if (q.x != 0) hi = max(hi, q.z);
+      if (tc.x != 0) hi = max(hi, fl.y);
     }
-    n32 = __reduce_add_sync(0xFFFFFFFFu, n32);
-    off = __reduce_add_sync(0xFFFFFFFFu, off);
+    n64 = warp_sum_u64(n64);
+    off = warp_sum_u64(off);
     const uint32_t my_lo = lo;
     lo = __reduce_min_sync(0xFFFFFFFFu, lo);
     hi = __reduce_max_sync(0xFFFFFFFFu, hi);
-    const uint32_t cdf_min32 = __reduce_add_sync(0xFFFFFFFFu, my_lo == lo ? lo_count : 0u);
-    uint32_t warp_off = 0;
+    const unsigned long long cdf_min64 = warp_sum_u64(my_lo == lo ? lo_count : 0ull);
+    unsigned long long warp_off = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       if (i < warp) warp_off += s_wsum[i];
@@ -749,8 +774,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       e1 = v0 + 1;
       if (w == 0) *stats = gpcx_lut_stats{0, 0, 0, 0};
     } else {
-      const std::uint64_t nn = n32;
-      const std::uint64_t cdf_min = cdf_min32;
+      const std::uint64_t nn = n64;
+      const std::uint64_t cdf_min = cdf_min64;
       if (w == 0) *stats = gpcx_lut_stats{nn, lo, hi, mode == GPCX_LUT_STRETCH ? 0 : cdf_min};
       if (mode == GPCX_LUT_STRETCH) {
         e0 = stretch_entry(v0, nn, lo, hi);
@@ -1055,7 +1080,7 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
   auto* base = static_cast<unsigned char*>(ws);
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
   auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
-  auto* blocks = reinterpret_cast<uint4*>(base + kBlocksOff);
+  auto* blocks = reinterpret_cast<SliceSummary*>(base + kBlocksOff);
   if (hist == nullptr) hist = reinterpret_cast<uint32_t*>(base + kHistOff);
   const int sms = device_sm_count();
   int nparts = parts_for(n, sms);

@@ -743,10 +743,12 @@ bool use_pair_kernel(std::uint64_t m, std::uint64_t n, std::uint64_t k, int sms)
   const char* force = std::getenv("GPCX_TC_KERNEL");
   if (force != nullptr && std::string(force) == "1sm") return false;
   if (force != nullptr && std::string(force) == "2sm") return true;
-  // Measured on B200 (tools/c4_ab.py, profiles/): the pair kernel wins at
-  // K <= 8192 (1115 vs 1039 TFLOP/s at 8192^3); at K = 32768 its operand
-  // panels hit L2 less (10.6 vs 4.6 GB of DRAM reads on 8192x8192x32768),
-  // the extra HBM power lowers the capped clock and the 1-SM kernel wins.
+  // Measured on B200 (tools/c4_ab.py, tools/gemm_sweep.sh, profiles/r1):
+  // the pair kernel wins at K <= 8192 (1115 vs 1039 TFLOP/s at 8192^3).
+  // With a 7-stage ring it lost at K = 32768 (its CTA pairs drifted apart
+  // and their shared panels fell out of L2: 10.6 vs 4.6 GB of DRAM reads
+  // on 8192x8192x32768); with the 4-stage ring it runs now it wins there
+  // too, so the choice depends on the tile count only, not on K.
   const std::uint64_t tiles2 = ((m + 255) / 256) * ((n + 255) / 256);
   (void)k;
   return m >= 256 && tiles2 >= static_cast<std::uint64_t>(sms / 2);

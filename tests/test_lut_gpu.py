@@ -209,18 +209,23 @@ def test_digest_matches_oracle(gpu):
 
 
 @pytest.mark.slow
-def test_c3_full_size_via_digest(gpu):
-    """32768^2 (config C3) LUT_CORRECT on one device; checked against the
-    oracle through the position-keyed digest (size-independent property)
-    plus the exact stats, and the equalize LUT's monotonicity."""
+@pytest.mark.parametrize("mode,mname", MODES)
+@pytest.mark.parametrize("kind", [O.IMG_RAMP12, O.IMG_UNIFORM16])
+def test_c3_full_size_via_digest(gpu, mode, mname, kind):
+    """32768^2 (config C3) LUT_CORRECT on one device, both modes, on the
+    bench scene (ramp12) and on uniform16 noise (the worst case for smem
+    bank conflicts): checked against the oracle through the position-keyed
+    digest (size-independent property) plus the exact LUT and stats."""
     torch, D = _dev()
     rows = cols = 32768
-    img = D.synth_image(O.IMG_RAMP12, 0x5EED, rows, cols)
+    img = D.synth_image(kind, 0x5EED, rows, cols)
     out = torch.empty_like(img)
     lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(img.numel())
-    D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+    D.lut_correct(img, out, mode, lut, stats, ws)
     host_img = u16(img)
-    r_out, r_lut, r_st = O.lut_correct(host_img, O.LUT_EQUALIZE)
+    del img
+    r_out, r_lut, r_st = O.lut_correct(host_img, mode)
+    del host_img
     assert np.array_equal(u16(lut), r_lut)
     assert D.read_stats(stats) == r_st
     assert int(D.digest_u16(out).item()) & (2 ** 64 - 1) == O.digest_u16(r_out)

@@ -118,6 +118,79 @@ def test_peer_exchange_equals_single_device_oracle(shared_gpu, tmp_path, nranks,
         assert sum(min(per, max(0, rows - r * per)) for r in range(nranks)) == rows
 
 
+_BIG_WORKER = r"""
+import json, os, sys, time
+from pathlib import Path
+import numpy as np, torch
+sys.path.insert(0, os.environ["GPCX_ROOT"])
+from paper_1505_05655_b200 import device as D
+rank, tmp, n, bulk = int(sys.argv[1]), Path(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+torch.cuda.set_device(0)
+# band: values 0..65535 once, then `bulk` for the remaining n - 65536 samples
+img = torch.full((n,), bulk, dtype=torch.int32, device="cuda").to(torch.int16)
+img[:65536] = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.int16)
+lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+p = D.LutPeer(rank, 2)
+(tmp / f"h{rank}.tmp").write_bytes(p.handle()); os.replace(tmp / f"h{rank}.tmp", tmp / f"h{rank}.bin")
+t0 = time.time()
+while not all((tmp / f"h{r}.bin").exists() for r in range(2)):
+    if time.time() - t0 > 60: raise SystemExit("peers never published their handles")
+    time.sleep(0.01)
+p.connect([(tmp / f"h{r}.bin").read_bytes() for r in range(2)])
+res = []
+for mode in (0, 1):
+    p.correct(img, img, mode, lut, stats, ws)   # in place
+    torch.cuda.synchronize()
+    l = lut.cpu().numpy().view(np.uint16)
+    # out = LUT[in] on the device, checked against the LUT the kernel built
+    head = img[:65536].cpu().numpy().view(np.uint16)
+    tail_ok = bool((img[65536:] == int(np.int16(np.uint16(l[bulk])))).all().item())
+    res.append({"stats": D.read_stats(stats), "lut": l.tobytes().hex(),
+                "head_ok": bool(np.array_equal(head, l)), "tail_ok": tail_ok})
+    # restore the band for the next mode
+    img.fill_(int(np.int16(np.uint16(bulk))))
+    img[:65536] = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.int16)
+(tmp / f"res{rank}.json").write_text(json.dumps(res))
+p.close()
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_peer_group_total_above_2_pow_32(shared_gpu, tmp_path):
+    """Two ranks of 2^31 + 2^20 samples each: the group's image holds more
+    than 2^32 pixels and one bin alone more than 2^32 counts, so the summed
+    histogram, its totals, cdf_min and stats.n must be 64-bit (each band's
+    own histogram is u32).  LUT and stats equal the oracle's from the exact
+    u64 group histogram; out == LUT[in] on every sample."""
+    from oracle import oracle as O
+    n, bulk = (1 << 31) + (1 << 20), 30000
+    env = dict(os.environ, GPCX_ROOT=str(ROOT), GPCX_PEER_TIMEOUT_MS="60000")
+    procs = [subprocess.Popen([sys.executable, "-c", _BIG_WORKER, str(r), str(tmp_path), str(n), str(bulk)],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    errs = []
+    for p in procs:
+        try:
+            _, err = p.communicate(timeout=300)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            _, err = p.communicate()
+        if p.returncode != 0:
+            errs.append(err[-3000:])
+    assert not errs, "\n".join(errs)
+    hist = np.full(65536, 2, dtype=np.uint64)
+    hist[bulk] += 2 * (n - 65536)
+    assert hist[bulk] > 2 ** 32 and hist.sum() > 2 ** 32
+    for r in range(2):
+        res = json.loads((tmp_path / f"res{r}.json").read_text())
+        for mode, rr in zip((O.LUT_EQUALIZE, O.LUT_STRETCH), res):
+            ref_lut, ref_st = O.lut_from_hist(hist, mode)
+            assert rr["stats"] == ref_st, (r, mode, rr["stats"], ref_st)
+            assert bytes.fromhex(rr["lut"]) == ref_lut.tobytes(), (r, mode)
+            assert rr["head_ok"] and rr["tail_ok"], (r, mode)
+
+
 _SILENT_PEER = r"""
 import os, sys, time
 from pathlib import Path

@@ -234,17 +234,18 @@ def test_tensor_core_operand_prep_strides(gpu, prec, pad_a, pad_b):
 
 
 @pytest.mark.slow
-def test_c4_full_size_sampled(gpu):
-    """Config C4 exactly as bench.py runs it (32768^3, prec=bf16, operands
-    synthesised on the device): sampled rows spread over all of C against
-    the f64 oracle on the same bf16-rounded operands."""
+@pytest.mark.parametrize("prec", [O.PREC_BF16, O.PREC_TF32])
+def test_c4_full_size_sampled(gpu, prec):
+    """Config C4 exactly as bench.py runs it (32768^3, prec=bf16 and its
+    tf32 variant, operands synthesised on the device): sampled rows spread
+    over all of C against the f64 oracle on the same rounded operands."""
     import torch
     from paper_1505_05655_b200 import device as D
     s = 32768
     A = D.synth_matrix(O.MAT_UNIFORM32, 0x5EED, s, s)
     B = D.synth_matrix(O.MAT_UNIFORM32, O.seed_b(0x5EED), s, s)
     Cm = torch.empty(s, s, device="cuda")
-    D.matmul(O.PREC_BF16, A, B, Cm, D.matmul_workspace(O.PREC_BF16, s, s, s))
+    D.matmul(prec, A, B, Cm, D.matmul_workspace(prec, s, s, s))
     rows = np.array([0, 255, 256, 12345, 20000, 32767])
     got = Cm[torch.from_numpy(rows).cuda()].cpu().numpy()
     a_rows = A[torch.from_numpy(rows).cuda()].cpu().numpy()
@@ -252,4 +253,4 @@ def test_c4_full_size_sampled(gpu):
     b = B.cpu().numpy()
     del B
     torch.cuda.empty_cache()
-    _check(got, a_rows, b, O.PREC_BF16)
+    _check(got, a_rows, b, prec)

@@ -205,6 +205,53 @@ def test_large_requests_overlap_receive_and_match(gpu, server):
 
 
 @pytest.mark.gpu
+@pytest.mark.slow
+def test_c5_chains_match_reference_server(gpu, server, refl):
+    """Config C5's chain at its full sizes (LUT_GEN -> LUT_APPLY of a 4096^2
+    u16 image, then MATMUL prec=bf16 4096^3 of the corrected image with B),
+    4 chains in flight, sent by the reference client to the B200 server and
+    to the reference server (acceptance.cpp:446-523: served bytes are the
+    same bytes): LUT_GEN / LUT_APPLY responses byte-identical, MATMUL
+    params identical and C within 1e-5 * sum|a||b| of the f64 oracle on the
+    bf16-rounded operands, for both servers."""
+    from oracle import oracle as O
+    side = 4096
+    dims = f"rows={side},cols={side}"
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(0x5EED), side, side)
+    imgs = [O.synth_image(O.IMG_RAMP12, 0x5EED + i, side, side) for i in range(4)]
+
+    def chain(port, img):
+        g = refl.ref_submit(port, "LUT_GEN", dims, img.tobytes(), "lut.bin")
+        a = refl.ref_submit(port, "LUT_APPLY", dims, g[2] + img.tobytes(), "img.raw")
+        A = np.frombuffer(a[2], dtype=np.uint16).reshape(side, side).astype(np.float32)
+        A *= np.float32(1.0 / 65535.0)
+        m = refl.ref_submit(port, "MATMUL", f"m={side},k={side},n={side},prec=bf16",
+                            A.tobytes() + B.tobytes(), "c.f32")
+        return g, a, m, A
+
+    def run_all(port):
+        import concurrent.futures as cf
+        with cf.ThreadPoolExecutor(max_workers=len(imgs)) as ex:
+            return list(ex.map(lambda im: chain(port, im), imgs))
+
+    ours = run_all(server.port)
+    with refl.RefServer(max_tasks=4) as rs:
+        theirs = run_all(rs.port)
+    rows = np.array([0, 1, 2047, 4095], dtype=np.uint64)
+    Br = O.round_matrix(O.PREC_BF16, B)
+    for img, (g, a, m, A), (g2, a2, m2, _) in zip(imgs, ours, theirs):
+        assert g[0] == "OK" and g == g2
+        assert a[0] == "OK" and a == a2
+        r_out, _, _ = O.lut_correct(img, O.LUT_EQUALIZE)
+        assert a[2] == r_out.tobytes()
+        assert m[0] == m2[0] == "OK" and m[1] == m2[1] and m[3] == m2[3] == "c.f32"
+        Cref, ab = O.matmul_f64(O.round_matrix(O.PREC_BF16, A), Br, rows)
+        for resp in (m, m2):
+            got = np.frombuffer(resp[2], dtype=np.float32).reshape(side, side)[rows.astype(np.int64)]
+            assert np.all(np.abs(got.astype(np.float64) - Cref) <= 1e-5 * ab + 1e-30)
+
+
+@pytest.mark.gpu
 def test_worker_and_device_count_invariance(gpu, refl):
     """acceptance.cpp:278-315 pattern (results independent of the worker
     count), carried to the B200 server: the same requests served with
