@@ -111,6 +111,18 @@ int gpcx_abi_version(void);
 int gpcx_init(int ndev, const int* devices);
 int gpcx_shutdown(void);
 int gpcx_device_count(int* count); /* devices bound (after init) */
+/* Health of bound device `index` (0 .. count-1): *healthy = 1 while the
+ * device takes work, 0 once quarantined after a sticky CUDA error (illegal
+ * address, launch failure / trap, ...): no request is routed to it any
+ * more and sharded requests use the remaining devices; with none left GPU
+ * tasks answer ERR:TASK_FAILED.  `why` (may be NULL) receives the error
+ * that caused the quarantine.  Rebinding with gpcx_init resets the state. */
+int gpcx_device_health(int index, int* healthy, char* why, uint64_t why_cap);
+/* Test hook for the health machinery: kind 0 quarantines bound index
+ * `index` without touching the GPU; kind 1 launches a kernel that traps on
+ * that device (a real sticky error, surfacing as TASK_FAILED here and at
+ * the device's next use).  Never called by the product paths. */
+int gpcx_debug_fault(int index, int kind);
 const char* gpcx_last_error(void);
 /* gpc::errc_name(Errc) for a status (proj/src/error.cpp:5-36). */
 const char* gpcx_status_name(int status);
@@ -291,12 +303,19 @@ int gpcx_digest_u16_device(const uint16_t* v, uint64_t n, uint64_t index0,
 
 /* ------------------------------------------------------------------ */
 /* Executor: the B200 task server (replaces srv::Server,               */
-/* proj/include/gpc/server.hpp:49-84, with pinned staging).             */
+/* proj/include/gpc/server.hpp:49-84).  Same wire contract; inside, a   */
+/* staged pipeline: epoll front end (header, one parse, admission       */
+/* control) -> payload receive into pinned staging -> one queue and     */
+/* worker group per bound GPU -> response send (csrc/host/server.hpp).  */
 /* ------------------------------------------------------------------ */
 
 /* Start a server on bind_addr:port (port 0 = ephemeral; *bound_port gets
  * the real one).  max_tasks <= 0 means 2 x hardware threads as in the
- * reference (server.cpp:114-119).  idle_timeout_ms <= 0 means 30000. */
+ * reference (server.cpp:114-119): the number of handlers running at once
+ * (split over the bound devices).  idle_timeout_ms <= 0 means 30000.  At
+ * most GPCX_MAX_PENDING (default max(64, 4 x max_tasks)) admitted requests
+ * are in progress; the next is answered ERR:TASK_FAILED, msg "server busy
+ * ..." before its payload is read. */
 int gpcx_server_start(const char* bind_addr, uint16_t port, int max_tasks,
                       int idle_timeout_ms, void** handle,
                       uint16_t* bound_port);
@@ -307,10 +326,12 @@ int gpcx_server_stop(void* handle);
 typedef struct gpcx_server_stats {
   uint64_t requests;
   double recv_ms, task_ms, send_ms;
+  uint64_t busy;     /* answered ERR:TASK_FAILED "server busy" by admission control */
+  uint64_t dropped;  /* connections closed without a response (idle, cut short, I/O) */
 } gpcx_server_stats;
 int gpcx_server_stats_get(void* handle, gpcx_server_stats* out);
-/* Serve one request held in memory, like srv::handle_connection over a
- * wire::MemoryStream (server.cpp:51-112).  Writes the response frame bytes
+/* Serve one request held in memory with the server's admission and error
+ * rules (the reference's handle_connection over a buffer, server.cpp:51-112).  Writes the response frame bytes
  * to resp (resp_cap must hold it; *resp_len = bytes needed).  Returns the
  * transport status (TRUNCATED for a cut-off request), 0 when answered. */
 int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp,

@@ -39,6 +39,7 @@ def devinfo_render(devices: list[DeviceInfo]) -> str:
 __all__ = [
     "GpcxError", "init", "shutdown", "device_count", "run", "payload_len", "output_len",
     "params_text", "parse_params", "Server", "handle_request", "flags", "required_params",
+    "device_health",
 ]
 
 
@@ -75,6 +76,14 @@ def device_count() -> int:
     n = C.c_int(0)
     check(lib.gpcx_device_count(C.byref(n)))
     return n.value
+
+
+def device_health(index: int) -> tuple[bool, str]:
+    """(healthy, reason) of bound device `index` (gpcx_device_health)."""
+    ok = C.c_int(0)
+    why = C.create_string_buffer(512)
+    check(lib.gpcx_device_health(index, C.byref(ok), why, 512))
+    return bool(ok.value), why.value.decode(errors="replace")
 
 
 def flags() -> list[str]:
@@ -170,7 +179,7 @@ class Server:
         st = ServerStats()
         check(lib.gpcx_server_stats_get(self._h, C.byref(st)))
         return {"requests": st.requests, "recv_ms": st.recv_ms, "task_ms": st.task_ms,
-                "send_ms": st.send_ms}
+                "send_ms": st.send_ms, "busy": st.busy, "dropped": st.dropped}
 
     def __enter__(self):
         return self.start()

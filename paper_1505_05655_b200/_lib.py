@@ -45,6 +45,7 @@ EXPORTS = [
     "gpcx_demosaic_device", "gpcx_devinfo_probe", "gpcx_devinfo_render", "gpcx_client_submit",
     "gpcx_lut_peer_create", "gpcx_lut_peer_ipc_handle", "gpcx_lut_peer_connect",
     "gpcx_lut_peer_destroy", "gpcx_lut_correct_peer_device", "gpcx_server_stats_get",
+    "gpcx_device_health", "gpcx_debug_fault",
 ]
 IPC_HANDLE_BYTES = 64
 
@@ -62,7 +63,7 @@ class DeviceInfo(C.Structure):
 
 class ServerStats(C.Structure):
     _fields_ = [("requests", C.c_uint64), ("recv_ms", C.c_double), ("task_ms", C.c_double),
-                ("send_ms", C.c_double)]
+                ("send_ms", C.c_double), ("busy", C.c_uint64), ("dropped", C.c_uint64)]
 
 
 class LutStats(C.Structure):
@@ -142,6 +143,8 @@ def _load() -> C.CDLL:
         "gpcx_lut_peer_destroy": ([vp], i32),
         "gpcx_lut_correct_peer_device": ([vp, vp, vp, u64, i32, vp, vp, vp, u64, vp], i32),
         "gpcx_server_stats_get": ([vp, vp], i32),
+        "gpcx_device_health": ([i32, C.POINTER(C.c_int), cp, u64], i32),
+        "gpcx_debug_fault": ([i32, i32], i32),
     }
     assert set(sig) == set(EXPORTS)
     for name, (args, res) in sig.items():

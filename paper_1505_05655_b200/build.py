@@ -38,7 +38,7 @@ CPP_SOURCES = [
     "host/peer.cpp",
     "host/devinfo.cpp",
     "host/registry.cpp",
-    "host/net.cpp",
+    "host/tcp.cpp",
     "host/server.cpp",
 ]
 

@@ -11,7 +11,7 @@
 #include "cuda_util.hpp"
 #include "host/devinfo.hpp"
 #include "host/executor.hpp"
-#include "host/net.hpp"
+#include "host/tcp.hpp"
 #include "host/peer.hpp"
 #include "host/registry.hpp"
 #include "host/runtime.hpp"
@@ -90,6 +90,30 @@ int gpcx_shutdown(void) {
 
 int gpcx_device_count(int* count) {
   return guarded([&] { *count = gpcx::rt::Runtime::get().ndev(); });
+}
+
+int gpcx_device_health(int index, int* healthy, char* why, uint64_t why_cap) {
+  return guarded([&] {
+    gpcx::rt::Runtime& R = gpcx::rt::Runtime::get();
+    if (index < 0 || index >= R.ndev()) gpcx::fail(gpcx::Errc::BadValue, "device index");
+    if (healthy != nullptr) *healthy = R.healthy(index) ? 1 : 0;
+    copy_text(R.health_reason(index), why, why_cap);
+  });
+}
+
+int gpcx_debug_fault(int index, int kind) {
+  return guarded([&] {
+    gpcx::rt::Runtime& R = gpcx::rt::Runtime::get();
+    if (index < 0 || index >= R.ndev()) gpcx::fail(gpcx::Errc::BadValue, "device index");
+    if (kind == 0) {
+      R.quarantine_index(index, "gpcx_debug_fault");
+      return;
+    }
+    if (kind != 1) gpcx::fail(gpcx::Errc::BadValue, "fault kind");
+    gpcx::rt::SlotLease s = R.acquire(index);
+    gpcx::synth::launch_trap(s->stream);
+    GPCX_CUDA(cudaStreamSynchronize(s->stream));  // fails: the trap is sticky
+  });
 }
 
 const char* gpcx_last_error(void) { return g_last_error.c_str(); }
@@ -506,7 +530,7 @@ int gpcx_server_stats_get(void* handle, gpcx_server_stats* out) {
     auto* h = static_cast<gpcx_server_handle*>(handle);
     if (h == nullptr || out == nullptr) gpcx::fail(gpcx::Errc::BadValue, "null argument");
     const gpcx::srv::ServerStats st = h->server->stats();
-    *out = gpcx_server_stats{st.requests, st.recv_ms, st.task_ms, st.send_ms};
+    *out = gpcx_server_stats{st.requests, st.recv_ms, st.task_ms, st.send_ms, st.busy, st.dropped};
   });
 }
 
@@ -516,7 +540,7 @@ int gpcx_handle_request(const uint8_t* req, uint64_t req_len, uint8_t* resp, uin
     static const gpcx::task::TaskRegistry* registry =
         new gpcx::task::TaskRegistry(gpcx::task::make_b200_registry());
     gpcx::wire::MemoryStream stream(std::vector<std::uint8_t>(req, req + req_len));
-    gpcx::srv::handle_connection(stream, *registry);
+    gpcx::srv::serve_stream(stream, *registry);
     const auto& bytes = stream.written();
     if (resp_len != nullptr) *resp_len = bytes.size();
     if (bytes.size() > resp_cap)
@@ -541,7 +565,7 @@ int gpcx_client_submit(const char* host, uint16_t port, const char* flag, const 
     h.data_marker = total > 0 ? gpcx::wire::kMarkerData : gpcx::wire::kMarkerNone;
     if (total > gpcx::wire::kMaxPayload) gpcx::fail(gpcx::Errc::TooLarge, "payload over the cap");
     const gpcx::wire::HeaderBytes raw = gpcx::wire::encode_header(h);
-    gpcx::net::Socket s = gpcx::net::Socket::connect_to(nz(host), port);
+    gpcx::tcp::Conn s = gpcx::tcp::dial(nz(host), port);
     s.write_all(raw);
     for (int i = 0; i < nparts; ++i)
       if (part_len[i] > 0)

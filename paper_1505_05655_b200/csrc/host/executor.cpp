@@ -29,6 +29,7 @@
 #include "../kernels.hpp"
 #include "devinfo.hpp"
 #include "runtime.hpp"
+#include "trace.hpp"
 
 namespace gpcx::exec {
 
@@ -53,7 +54,9 @@ struct InflightGuard {
 
 std::vector<Band> plan_bands(std::uint64_t rows, std::uint64_t work, std::uint64_t threshold) {
   rt::Runtime& R = rt::Runtime::get();
-  const int ndev = R.ndev();
+  // shards go to the healthy devices only (a quarantined one takes no work)
+  const std::vector<int> live = R.healthy_indices();
+  const int ndev = static_cast<int>(live.size());
   if (ndev <= 1 || work < threshold || rows < 2 || g_inflight.load() > 1)
     return {Band{R.pick_device_index(), 0, rows}};
   const std::uint64_t g = std::min<std::uint64_t>(static_cast<std::uint64_t>(ndev), rows);
@@ -62,7 +65,7 @@ std::vector<Band> plan_bands(std::uint64_t rows, std::uint64_t work, std::uint64
   for (std::uint64_t i = 0; i < g; ++i) {
     const std::uint64_t r0 = i * per;
     if (r0 >= rows) break;
-    bands.push_back(Band{static_cast<int>(i), r0, std::min(per, rows - r0)});
+    bands.push_back(Band{live[i], r0, std::min(per, rows - r0)});
   }
   return bands;
 }
@@ -189,6 +192,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     const Band& b = bands[i];
     const std::uint64_t bn = b.nrows * p.cols;
     auto* dimg = s.a.as<std::uint16_t>();
+    const obs::Range range("kernel");
     if (flag != Flag::LutApply) {
       if (G == 1) {
         if (equalize && need_apply) {  // one fused launch: histogram -> LUT -> apply
@@ -287,6 +291,7 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
                                     peer.b.as<std::uint8_t>() + ks[j] * row_bytes, peer.device,
                                     (ks[j + 1] - ks[j]) * row_bytes, s.stream));
     }
+    const obs::Range range("kernel");
     if (p.prec == GPCX_PREC_F32) {
       const std::uint64_t wsb = gemm::sgemm_workspace_bytes(b.nrows, p.n, p.k);
       if (wsb != 0) s.mm_ws.ensure(wsb);
@@ -331,6 +336,7 @@ void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* 
     s.a.ensure((in1 - in0) * p.cols * 2);
     s.c.ensure(bn * 6);
     rt::h2d(s, s.a.ptr, in + in0 * p.cols, (in1 - in0) * p.cols * 2);
+    const obs::Range range("kernel");
     demosaic::launch_band(gradient, p.phase, s.a.as<std::uint16_t>(), s.c.as<std::uint16_t>(),
                           p.rows, p.cols, b.row0, in0, b.nrows, s.stream);
     for (int k = 0; k < 3; ++k)  // R, G, B planes of the band
@@ -408,6 +414,11 @@ wire::ParamMap execute(Flag flag, const wire::ParamMap& params,
   if (in.size() != want_in)
     fail(Errc::PayloadMismatch,
          "payload is " + std::to_string(in.size()) + " bytes, want " + std::to_string(want_in));
+  return execute_admitted(flag, params, in, out);
+}
+
+wire::ParamMap execute_admitted(Flag flag, const wire::ParamMap& params,
+                                std::span<const std::uint8_t> in, std::span<std::uint8_t> out) {
   wire::ParamMap result;
   if (flag == Flag::DevInfo) {
     const std::string& xml = devinfo_xml();

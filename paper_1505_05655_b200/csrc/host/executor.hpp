@@ -19,6 +19,10 @@ namespace gpcx::exec {
 // least task::output_len().  Returns the result params (without bytes=).
 wire::ParamMap execute(task::Flag flag, const wire::ParamMap& params,
                        std::span<const std::uint8_t> in, std::span<std::uint8_t> out);
+// The same for a request the registry already admitted (task::admit): its
+// payload length was checked there, so it is not recomputed.
+wire::ParamMap execute_admitted(task::Flag flag, const wire::ParamMap& params,
+                                std::span<const std::uint8_t> in, std::span<std::uint8_t> out);
 
 // The same, on typed host buffers and without the wire's 1 GiB cap (the
 // in-process entry points gpcx_lut_host / gpcx_matmul_host).

@@ -57,42 +57,66 @@ std::string sanitize_message(std::string_view text, const wire::ParamMap& existi
   return msg;
 }
 
-DispatchResult dispatch(const TaskRegistry& registry, const RequestView& request) {
-  DispatchResult result;
-  auto fail_with = [&](const std::string& code, const char* what) {
-    result.status = "ERR:" + code;
-    result.params = wire::ParamMap();
-    result.params.set("msg", sanitize_message(what, result.params));
-    result.output = TaskOutput{};
-  };
+Admission admit(const TaskRegistry& registry, const wire::TaskHeader& h) {
+  Admission a;
+  a.descriptor = &registry.lookup(h.task_flag);
+  a.params = wire::ParamMap::parse(h.params);
+  for (const std::string& key : a.descriptor->required_params)
+    if (!a.params.has(key)) fail(Errc::MissingParam, key);
+  a.payload_len = a.descriptor->payload_rule(a.params);
+  const bool marked = h.data_marker == wire::kMarkerData;
+  if (marked && a.payload_len == 0)
+    fail(Errc::PayloadMismatch, "marker promises payload, expected length 0");
+  if (!marked && a.payload_len > 0)
+    fail(Errc::PayloadMismatch,
+         "no payload marker, expected " + std::to_string(a.payload_len) + " bytes");
+  return a;
+}
+
+namespace {
+DispatchResult failure(const std::string& code, const char* what) {
+  DispatchResult r;
+  r.status = "ERR:" + code;
+  r.params.set("msg", sanitize_message(what, r.params));
+  return r;
+}
+}  // namespace
+
+DispatchResult error_result(Errc code, std::string_view what) {
+  return failure(gpcx::response_code(code), std::string(what).c_str());
+}
+
+DispatchResult run_admitted(const Admission& a, std::span<const std::uint8_t> payload) {
   try {
-    const wire::TaskHeader& h = *request.header;
-    const TaskDescriptor& d = registry.lookup(h.task_flag);
-    const wire::ParamMap params = wire::ParamMap::parse(h.params);
-    for (const std::string& key : d.required_params)
-      if (!params.has(key)) fail(Errc::MissingParam, key);
-    const std::uint64_t want = d.payload_rule(params);
-    const bool marked = h.data_marker == wire::kMarkerData;
-    if (marked && want == 0)
-      fail(Errc::PayloadMismatch, "marker promises payload, expected length 0");
-    if (!marked && want > 0)
-      fail(Errc::PayloadMismatch, "no payload marker, expected " + std::to_string(want) + " bytes");
-    if (request.payload.size() != want)
-      fail(Errc::PayloadMismatch, "payload is " + std::to_string(request.payload.size()) +
-                                      " bytes, want " + std::to_string(want));
-    result.output = d.handler(params, request.payload);
-    result.params = std::move(result.output.params);
-    result.output.params = wire::ParamMap();
-    result.params.set("bytes", static_cast<std::uint64_t>(result.output.bytes().size()));
-    result.status = "OK";
+    if (payload.size() != a.payload_len)
+      fail(Errc::PayloadMismatch, "payload is " + std::to_string(payload.size()) +
+                                      " bytes, want " + std::to_string(a.payload_len));
+    DispatchResult r;
+    r.output = a.descriptor->handler(a.params, payload);
+    r.params = std::move(r.output.params);
+    r.output.params = wire::ParamMap();
+    r.params.set("bytes", static_cast<std::uint64_t>(r.output.bytes().size()));
+    r.status = "OK";
+    return r;
   } catch (const Error& e) {
-    fail_with(gpcx::response_code(e.code()), e.what());
+    return failure(gpcx::response_code(e.code()), e.what());
   } catch (const std::exception& e) {
-    fail_with("TASK_FAILED", e.what());
+    return failure("TASK_FAILED", e.what());
   } catch (...) {
-    fail_with("TASK_FAILED", "unknown failure");
+    return failure("TASK_FAILED", "unknown failure");
   }
-  return result;
+}
+
+DispatchResult dispatch(const TaskRegistry& registry, const RequestView& request) {
+  Admission a;
+  try {
+    a = admit(registry, *request.header);
+  } catch (const Error& e) {
+    return failure(gpcx::response_code(e.code()), e.what());
+  } catch (const std::exception& e) {
+    return failure("TASK_FAILED", e.what());
+  }
+  return run_admitted(a, request.payload);
 }
 
 wire::TaskHeader make_response_header(const DispatchResult& result, std::string_view output_name) {
@@ -119,7 +143,8 @@ TaskRegistry make_b200_registry() {
           f == Flag::DevInfo ? exec::devinfo_xml().size() : output_len(f, p);
       out.pinned = rt::pinned_acquire(len);
       out.pinned_len = len;
-      out.params = exec::execute(
+      // admitted: payload length already checked against this rule
+      out.params = exec::execute_admitted(
           f, p, in, std::span<std::uint8_t>(static_cast<std::uint8_t*>(out.pinned.get()), len));
       return out;
     };

@@ -72,6 +72,27 @@ struct RequestView {
   std::span<const std::uint8_t> payload;
 };
 
+// The one parse of a request header: descriptor lookup,
+// params, required keys, payload length from the descriptor's rule and the
+// marker check -- what the reference does twice, in handle_connection
+// (proj/src/server.cpp:73-93) and again in dispatch (registry.cpp:83-90).
+// The front end admits a request once, sizes its staging from
+// payload_len, and runs it with run_admitted.  Throws gpcx::Error.
+struct Admission {
+  const TaskDescriptor* descriptor = nullptr;
+  wire::ParamMap params;
+  std::uint64_t payload_len = 0;
+};
+Admission admit(const TaskRegistry& registry, const wire::TaskHeader& header);
+
+// Runs an admitted request's handler on its payload; never throws (every
+// failure becomes ERR:<CODE>, proj/src/registry.cpp:98-120).
+DispatchResult run_admitted(const Admission& admission, std::span<const std::uint8_t> payload);
+
+// A failure result: ERR:<CODE> with the sanitised msg= (no payload).
+DispatchResult error_result(Errc code, std::string_view what);
+
+// admit + run_admitted (the reference's dispatch contract, one parse).
 DispatchResult dispatch(const TaskRegistry& registry, const RequestView& request);
 inline DispatchResult dispatch(const TaskRegistry& registry, const wire::Frame& request) {
   return dispatch(registry, RequestView{&request.header, request.payload});

@@ -2,6 +2,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -10,10 +11,45 @@
 
 #include "../cuda_util.hpp"
 #include "../kernels.hpp"
+#include "trace.hpp"
 
 namespace gpcx::rt {
 
 void use_device(int device) { GPCX_CUDA(cudaSetDevice(device)); }
+
+namespace {
+thread_local int t_affinity = -1;
+}  // namespace
+
+Affinity::Affinity(int index) : saved_(t_affinity) { t_affinity = index; }
+Affinity::~Affinity() { t_affinity = saved_; }
+
+bool is_sticky(cudaError_t e) {
+  switch (e) {
+    case cudaErrorIllegalAddress:
+    case cudaErrorLaunchFailure:  // includes __trap()
+    case cudaErrorIllegalInstruction:
+    case cudaErrorMisalignedAddress:
+    case cudaErrorInvalidAddressSpace:
+    case cudaErrorInvalidPc:
+    case cudaErrorHardwareStackError:
+    case cudaErrorAssert:
+    case cudaErrorLaunchTimeout:
+    case cudaErrorECCUncorrectable:
+    case cudaErrorContextIsDestroyed:
+      return true;
+    default:
+      return false;
+  }
+}
+
+void note_cuda_error(cudaError_t e, const char* where) {
+  if (!is_sticky(e)) return;
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return;
+  Runtime::get().quarantine_device(
+      dev, std::string(cudaGetErrorName(e)) + " at " + (where != nullptr ? where : "?"));
+}
 
 void DeviceBuf::ensure(std::uint64_t bytes, bool zero) {
   if (bytes <= cap && ptr != nullptr) return;
@@ -113,7 +149,15 @@ void Runtime::init(const std::vector<int>& devices) {
   if (want.empty()) fail(Errc::TaskFailed, "no CUDA device available");
   std::vector<int> have;
   for (const Pool& p : pools_) have.push_back(p.device);
-  if (inited_ && have == want) return;
+  if (inited_ && have == want) {
+    // same set: quarantined devices are admitted again (if the context is
+    // still broken, its next sticky error quarantines it again)
+    for (Pool& p : pools_) {
+      p.healthy = true;
+      p.why.clear();
+    }
+    return;
+  }
   pools_.clear();
   for (int d : want) {
     int count = 0;
@@ -158,14 +202,83 @@ int Runtime::device_at(int index) { return devices().at(static_cast<std::size_t>
 int Runtime::ndev() { return static_cast<int>(devices().size()); }
 
 int Runtime::pick_device_index() {
-  const int n = ndev();
-  return static_cast<int>(rr_.fetch_add(1) % static_cast<unsigned>(n));
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  const int n = static_cast<int>(pools_.size());
+  if (t_affinity >= 0 && t_affinity < n && pools_[t_affinity].healthy) return t_affinity;
+  // round robin over the healthy devices
+  for (int tries = 0; tries < n; ++tries) {
+    const int i = static_cast<int>(rr_.fetch_add(1) % static_cast<unsigned>(n));
+    if (pools_[i].healthy) return i;
+  }
+  std::string why = "no healthy device:";
+  for (const Pool& p : pools_) why += " device " + std::to_string(p.device) + " quarantined (" + p.why + ");";
+  fail(Errc::TaskFailed, why);
+}
+
+std::vector<int> Runtime::healthy_indices() {
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  std::vector<int> out;
+  for (std::size_t i = 0; i < pools_.size(); ++i)
+    if (pools_[i].healthy) out.push_back(static_cast<int>(i));
+  return out;
+}
+
+bool Runtime::healthy(int index) {
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  return pools_.at(static_cast<std::size_t>(index)).healthy;
+}
+
+std::string Runtime::health_reason(int index) {
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  return pools_.at(static_cast<std::size_t>(index)).why;
+}
+
+// Idle slots of a quarantined device are destroyed (their CUDA frees fail
+// quietly on the dead context; the host-side objects go).
+void Runtime::retire_idle_locked(Pool& pool) {
+  for (Slot* s : pool.free) {
+    for (std::size_t k = 0; k < pool.all.size(); ++k) {
+      if (pool.all[k].get() == s) {
+        pool.all.erase(pool.all.begin() + static_cast<std::ptrdiff_t>(k));
+        break;
+      }
+    }
+  }
+  pool.free.clear();
+  cudaGetLastError();
+}
+
+void Runtime::quarantine_device(int ordinal, const std::string& why) {
+  std::lock_guard<std::mutex> lock(mu_);
+  for (Pool& p : pools_) {
+    if (p.device != ordinal || !p.healthy) continue;
+    p.healthy = false;
+    p.why = why;
+    retire_idle_locked(p);
+    std::fprintf(stderr, "gpcx: device %d quarantined after %s\n", ordinal, why.c_str());
+  }
+}
+
+void Runtime::quarantine_index(int index, const std::string& why) {
+  std::lock_guard<std::mutex> lock(mu_);
+  ensure_init_locked();
+  Pool& p = pools_.at(static_cast<std::size_t>(index));
+  if (!p.healthy) return;
+  p.healthy = false;
+  p.why = why;
+  retire_idle_locked(p);
 }
 
 SlotLease Runtime::acquire(int device_index) {
   std::unique_lock<std::mutex> lock(mu_);
   ensure_init_locked();
   Pool& pool = pools_.at(static_cast<std::size_t>(device_index));
+  if (!pool.healthy)
+    fail(Errc::TaskFailed, "device " + std::to_string(pool.device) + " quarantined (" + pool.why + ")");
   if (!pool.free.empty()) {
     Slot* s = pool.free.back();
     pool.free.pop_back();
@@ -195,11 +308,11 @@ void Runtime::release(Slot* slot) {
   std::lock_guard<std::mutex> lock(mu_);
   for (Pool& p : pools_) {
     if (p.device != slot->device) continue;
-    for (auto& owned : p.all) {
-      if (owned.get() == slot) {
-        p.free.push_back(slot);
-        return;
-      }
+    for (std::size_t k = 0; k < p.all.size(); ++k) {
+      if (p.all[k].get() != slot) continue;
+      if (p.healthy) p.free.push_back(slot);
+      else p.all.erase(p.all.begin() + static_cast<std::ptrdiff_t>(k));  // retired
+      return;
     }
   }
   // Pool was rebuilt while the slot was leased: the unique_ptr that owned it
@@ -218,7 +331,18 @@ PinnedPool& pinned_pool() {
   return *p;
 }
 constexpr std::uint64_t kPinnedIdleCap = 8ull << 30;
+std::atomic<std::uint64_t> g_pinned_in_use{0};
+std::uint64_t pinned_cap() {
+  static const std::uint64_t cap = [] {
+    const char* v = std::getenv("GPCX_PINNED_CAP_MB");
+    const long long mb = v != nullptr ? std::atoll(v) : 0;
+    return mb > 0 ? static_cast<std::uint64_t>(mb) << 20 : 32ull << 30;
+  }();
+  return cap;
+}
 }  // namespace
+
+std::uint64_t pinned_in_use() { return g_pinned_in_use.load(); }
 
 PinnedLease& PinnedLease::operator=(PinnedLease&& o) noexcept {
   if (this != &o) {
@@ -238,6 +362,7 @@ PinnedLease::~PinnedLease() {
     ptr_ = nullptr;
     return;
   }
+  g_pinned_in_use.fetch_sub(cap_);
   PinnedPool& pool = pinned_pool();
   std::lock_guard<std::mutex> lock(pool.mu);
   if (pool.idle_bytes + cap_ > kPinnedIdleCap) {
@@ -252,6 +377,14 @@ PinnedLease::~PinnedLease() {
 PinnedLease pinned_acquire(std::uint64_t bytes) {
   std::uint64_t cls = 4096;
   while (cls < bytes) cls <<= 1;
+  // over the page-locked budget: a heap lease (staged through the slots'
+  // pinned bounce buffers by h2d / d2h)
+  if (g_pinned_in_use.fetch_add(cls) + cls > pinned_cap()) {
+    g_pinned_in_use.fetch_sub(cls);
+    void* p = std::malloc(cls);
+    if (p == nullptr) fail(Errc::TaskFailed, "out of host memory");
+    return PinnedLease(p, cls, /*pageable=*/true);
+  }
   PinnedPool& pool = pinned_pool();
   {
     std::lock_guard<std::mutex> lock(pool.mu);
@@ -267,6 +400,7 @@ PinnedLease pinned_acquire(std::uint64_t bytes) {
   void* p = nullptr;
   if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
     cudaGetLastError();
+    g_pinned_in_use.fetch_sub(cls);
     p = std::malloc(cls);
     if (p == nullptr) fail(Errc::TaskFailed, "out of host memory");
     return PinnedLease(p, cls, /*pageable=*/true);
@@ -352,6 +486,7 @@ void Arrival::wait_for(std::uint64_t upto) {
 
 void h2d(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
   if (bytes == 0) return;
+  const obs::Range range("h2d");
   if (Arrival* a = find_arrival(src)) {  // payload still arriving: chunk as it lands
     const std::uint64_t start = static_cast<std::uint64_t>(static_cast<const std::uint8_t*>(src) - a->base());
     const auto* in = static_cast<const std::uint8_t*>(src);
@@ -384,6 +519,7 @@ void h2d(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
 }
 
 void d2h(Slot& s, void* dst, const void* src, std::uint64_t bytes) {
+  const obs::Range range("d2h");
   if (bytes == 0) {
     GPCX_CUDA(cudaStreamSynchronize(s.stream));
     return;

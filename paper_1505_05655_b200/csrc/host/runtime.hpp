@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../../include/gpcx.h"
@@ -89,6 +90,39 @@ class SlotLease {
   Slot* slot_;
 };
 
+// Thread-local device affinity: while alive, pick_device_index() on this
+// thread returns `index` (the server's per-device workers), as long as that
+// device is healthy.
+class Affinity {
+ public:
+  explicit Affinity(int index);
+  ~Affinity();
+  Affinity(const Affinity&) = delete;
+  Affinity& operator=(const Affinity&) = delete;
+
+ private:
+  int saved_;
+};
+
+// Device health (SURVEY.md §5 failure detection; the reference's failure
+// boundary is the handler exception -> ERR:TASK_FAILED, proj/src/
+// registry.cpp:113-118).  A sticky CUDA error (illegal address, launch
+// failure, trap, ...) poisons the device's context for the whole process:
+// every later call on it fails.  The runtime therefore QUARANTINES the
+// device -- its idle slots are retired, leased ones are not returned, no new
+// request is routed to it, the planner shards only over healthy devices --
+// and requests keep running on the remaining ones; only when none is left
+// does every GPU request answer ERR:TASK_FAILED ("no healthy device").  The
+// request that hit the fault fails (it is not retried elsewhere: a fault its
+// data caused would poison the next device too).  A quarantined device is
+// not reset in-process (cudaDeviceReset would free pinned host buffers and
+// peer mappings other devices' work still uses); rebinding with gpcx_init or
+// restarting the server process brings it back.
+bool is_sticky(cudaError_t e);
+// Called on every failed CUDA call (GPCX_CUDA): quarantines the calling
+// thread's current device when `e` is sticky.
+void note_cuda_error(cudaError_t e, const char* where);
+
 class Runtime {
  public:
   static Runtime& get();
@@ -98,7 +132,14 @@ class Runtime {
   void shutdown();
   std::vector<int> devices();
   int ndev();
-  int pick_device_index();  // round robin over bound devices (C5 replicas)
+  // The thread's affinity if set and healthy, else round robin over the
+  // healthy bound devices (C5 replicas); TaskFailed when none is healthy.
+  int pick_device_index();
+  std::vector<int> healthy_indices();
+  bool healthy(int index);
+  std::string health_reason(int index);  // "" while healthy
+  void quarantine_device(int ordinal, const std::string& why);  // every index bound to it
+  void quarantine_index(int index, const std::string& why);     // one bound index (tests)
   // Device ordinal of bound index i.
   int device_at(int index);
   SlotLease acquire(int device_index);
@@ -109,7 +150,10 @@ class Runtime {
     int device;
     std::vector<std::unique_ptr<Slot>> all;
     std::vector<Slot*> free;
+    bool healthy = true;
+    std::string why;  // first sticky error seen on it
   };
+  void retire_idle_locked(Pool& pool);
   void ensure_init_locked();
   std::mutex mu_;
   bool inited_ = false;
@@ -172,9 +216,14 @@ class PinnedLease {
   std::uint64_t cap_ = 0;
   bool pageable_ = false;  // page-locking unavailable (no usable device)
 };
-// A pooled pinned buffer; when page-locking fails (no usable device) a plain
-// heap buffer, so framing still works and the handler reports the GPU error.
+// A pooled pinned buffer.  Page-locked bytes leased at once are bounded
+// (GPCX_PINNED_CAP_MB, default 32 GiB): past the bound -- e.g. many clients
+// that sent only headers of large requests -- a lease is plain heap memory,
+// which the staging copies handle through their chunked pinned bounce
+// buffers.  When page-locking fails (no usable device) also a heap buffer,
+// so framing still works and the handler reports the GPU error.
 PinnedLease pinned_acquire(std::uint64_t bytes);
+std::uint64_t pinned_in_use();  // page-locked bytes currently leased
 void pinned_trim();  // frees idle pooled buffers
 
 // Makes `device` current for the calling thread.

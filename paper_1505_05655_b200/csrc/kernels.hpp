@@ -136,6 +136,8 @@ void launch_matrix(int kind, std::uint64_t seed, std::uint64_t rows,
 void launch_digest(const std::uint16_t* v, std::uint64_t n,
                    std::uint64_t index0, std::uint64_t* digest,
                    cudaStream_t stream);
+// A kernel that executes __trap() (gpcx_debug_fault: a real sticky error).
+void launch_trap(cudaStream_t stream);
 }  // namespace synth
 
 namespace gemm {

@@ -358,3 +358,37 @@ def test_server_phase_stats_count_answered_requests(refl):
         st = s.stats()
         assert st["requests"] == 5
         assert all(st[k] >= 0.0 for k in ("recv_ms", "task_ms", "send_ms"))
+
+
+def test_admission_control_answers_busy_early(monkeypatch, refl):
+    """The bounded pipeline: with GPCX_MAX_PENDING=1, a request admitted and
+    still receiving its payload holds the only place; the next valid request
+    is answered ERR:TASK_FAILED ("server busy") at once, before any payload
+    byte (the reference queues it in an unbounded deque, server.hpp:81).
+    Once the first one is answered the server admits again."""
+    monkeypatch.setenv("GPCX_MAX_PENDING", "1")
+    with G.Server(max_tasks=2, idle_timeout_ms=5000) as s:
+        hold = socket.create_connection(("127.0.0.1", s.port), timeout=10)
+        hold.sendall(W.header("LUT_CORRECT", "rows=64,cols=64", has_payload=True) + b"\0" * 100)
+        time.sleep(0.3)  # admitted, receiving
+        status, params, _, name = refl.ref_submit(s.port, "LUT_CORRECT", "rows=64,cols=64",
+                                                  b"\0" * 8192, "busy.raw")
+        assert status == "ERR:TASK_FAILED" and name == "busy.raw"
+        assert G.parse_params(params)["msg"].startswith("server busy")
+        hold.sendall(b"\0" * (8192 - 100))  # completes: answered (TASK_FAILED without a GPU)
+        hold.settimeout(30)
+        assert W.parse_response(hold.recv(4096))["status"].startswith(("OK", "ERR:"))
+        hold.close()
+        status, _, _, _ = refl.ref_submit(s.port, "NOPE", "", b"", "a")
+        assert status == "ERR:UNKNOWN_TASK"
+        st = s.stats()
+        assert st["busy"] == 1
+
+
+def test_dropped_connections_are_counted(server):
+    before = server.stats()["dropped"]
+    with socket.create_connection(("127.0.0.1", server.port), timeout=10) as c:
+        c.sendall(b"LUT_")
+        assert c.recv(16) == b""  # dropped at the 300 ms idle timeout, no response
+    time.sleep(0.1)
+    assert server.stats()["dropped"] >= before + 1

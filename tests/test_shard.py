@@ -127,3 +127,41 @@ def test_peer_exchange_negotiation_is_unanimous(fail_at):
         assert got == {0: [0, 1], 1: [0, 1]}
     else:
         assert got == {0: None, 1: None}
+
+
+def _mm_worker(rank, world, port, m, k, n, q):
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as O
+    from paper_1505_05655_b200.shard import ShardedMatmul
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r0, nr = band(m, world, rank)
+    k0, nk = band(k, world, rank)
+    a = torch.from_numpy(O.synth_matrix(O.MAT_UNIFORM32, 9, m, k, r0, nr))
+    b = torch.from_numpy(O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(9), k, n, k0, nk))
+    c = ShardedMatmul(dist, lambda A, B: torch.from_numpy(O.matmul_f32(A.numpy(), B.numpy()))).run(
+        a, b, k, n, world)
+    full = gather_bands(dist, c, [nr_ for _, nr_ in bands(m, world)], n)
+    if rank == 0:
+        q.put(full.numpy().tobytes())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,k,n", [(2, 64, 96, 40), (3, 67, 101, 33)])
+def test_sharded_matmul_over_gloo_equals_single_process(world, m, k, n):
+    """Block rows of A / C per rank, B replicated from per-rank k-slices
+    (equal slices: all-gather; ragged: per-owner broadcasts), C gathered
+    with exact sizes: bitwise equal to the single-process product."""
+    from oracle import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mm_worker, args=(r, world, port, m, k, n, q)) for r in range(world)]
+    [p.start() for p in procs]
+    got = q.get(timeout=120)
+    [p.join(timeout=60) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    A = O.synth_matrix(O.MAT_UNIFORM32, 9, m, k)
+    B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(9), k, n)
+    assert got == O.matmul_f32(A, B).tobytes()
