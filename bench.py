@@ -408,38 +408,99 @@ def lut_e2e_leg(n_gpus: int, steps: int, warmup: int, mode: int, inflight: int =
             "h2d_bytes_per_step": n * 2, "d2h_bytes_per_step": n * 2, "inflight": inflight}
 
 
-MM4 = 32768  # config C4
+# config C4 (GPCX_BENCH_MM4 shrinks it for the GPCX_BENCH_ONE_GPU dry run
+# only: 8 ranks replicating a 4 GiB B over gloo through host memory)
+MM4 = int(os.environ.get("GPCX_BENCH_MM4", "32768")) if os.environ.get("GPCX_BENCH_ONE_GPU") == "1" \
+    else 32768
 C4_SAMPLE_ROWS, C4_SAMPLE_COLS = 128, 512  # CPU baseline / parity sample of C
 
 
 def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
     """Config C4: 32768^3 MATMUL on the tcgen05 path, block rows of A / C per
-    rank, B replicated (generated in place on every rank: the broadcast is
-    not part of the per-step work).  One step = the rank's whole block-row
-    product including the f32 -> bf16 operand preparation."""
+    rank.  B is REPLICATED every step: rank r holds only its
+    k-slice of B's rows (generated in place -- what its own PCIe link would
+    stage) and the slices are all-gathered (NCCL over NVLink;
+    shard.replicate_rows) into a double-buffered full B on a side stream, so
+    step s+1's replication runs under step s's GEMM.  One step = replicate
+    B + the rank's block-row product including the f32 -> bf16 operand
+    preparation.  `ms` is that pipelined step; `compute_ms` the product
+    alone; `replicate_ms` one replication timed by itself (N>1)."""
     import torch
     from paper_1505_05655_b200 import device as D
+    from paper_1505_05655_b200.shard import replicate_rows
     r0, nr = band(MM4, d.n, d.rank)
+    k0, nk = band(MM4, d.n, d.rank)
+    kslices = [band(MM4, d.n, r)[1] for r in range(d.n)]
     A = D.synth_matrix(1, SEED, MM4, MM4, r0, nr)
-    B = D.synth_matrix(1, SEED_B, MM4, MM4)
     Cm = torch.empty(nr, MM4, device="cuda")
     ws = D.matmul_workspace(prec, nr, MM4, MM4)
     stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        D.matmul(prec, A, B, Cm, ws, stream)
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    sharded = d.pg is not None
+    if sharded:
+        own = D.synth_matrix(1, SEED_B, MM4, MM4, k0, nk)
+        bufs = [torch.empty(MM4, MM4, device="cuda") for _ in range(2)]
+        comm = torch.cuda.Stream()
+    else:  # one rank owns all of B: nothing to replicate
+        bufs = [D.synth_matrix(1, SEED_B, MM4, MM4)]
+
+    def replicate(buf, after=None):
+        with torch.cuda.stream(comm):
+            if after is not None:
+                comm.wait_event(after)
+            replicate_rows(d.pg, own, kslices, MM4, out=buf)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+        return ev
+
+    def run(n_steps: int, record: bool):
+        """n_steps pipelined steps; returns per-step compute events."""
+        done = [None, None]
+        ready = replicate(bufs[0]) if sharded else None
+        spans = []
+        for s in range(n_steps):
+            b = bufs[s % len(bufs)]
+            if ready is not None:
+                stream.wait_event(ready)
+            if sharded and s + 1 < n_steps:  # next step's B, under this GEMM
+                ready = replicate(bufs[(s + 1) % 2], after=done[(s + 1) % 2])
+            a0 = E() if record else None
+            if record:
+                a0.record(stream)
+            D.matmul(prec, A, b, Cm, ws, stream)
+            ev = torch.cuda.Event(enable_timing=record)
+            ev.record(stream)
+            done[s % 2] = ev
+            if record:
+                spans.append((a0, ev))
+        return spans
+
+    run(warmup, False)
     torch.cuda.synchronize()
     d.barrier()
     torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0, t1 = E(), E()
     with Clocks(d.gpu) as clk:
         t0.record(stream)
-        for _ in range(steps):
-            D.matmul(prec, A, B, Cm, ws, stream)
+        spans = run(steps, True)
         t1.record(stream)
         torch.cuda.synchronize()
     d.barrier()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
+    compute_ms = sum(a.elapsed_time(b) for a, b in spans) / steps
+    rep_ms = None
+    if sharded:  # one replication by itself (not under a GEMM)
+        d.barrier()
+        torch.cuda.synchronize()
+        a, b = E(), E()
+        a.record(comm)
+        with torch.cuda.stream(comm):
+            replicate_rows(d.pg, own, kslices, MM4, out=bufs[0])
+        b.record(comm)
+        torch.cuda.synchronize()
+        rep_ms = a.elapsed_time(b)
+    B = bufs[(steps - 1) % len(bufs)]
     # rank 0 keeps a 128 x 512 corner of the product (and its operands) for
     # the CPU baseline and a sampled parity check against the f64 oracle
     sample = None
@@ -447,7 +508,9 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
         sample = {"A": A[:C4_SAMPLE_ROWS].cpu().numpy(),
                   "B": B[:, :C4_SAMPLE_COLS].contiguous().cpu().numpy(),
                   "C": Cm[:C4_SAMPLE_ROWS, :C4_SAMPLE_COLS].cpu().numpy(), "prec": prec}
-    del A, B, ws
+    del A, B, ws, bufs
+    if sharded:
+        del own
     gather_ms = None
     if d.pg is not None:  # the C bands to rank 0, timed apart from the compute
         from paper_1505_05655_b200.shard import gather_bands
@@ -464,8 +527,8 @@ def matmul_c4_leg(d: Dist, steps: int, warmup: int, prec: int = 2) -> dict:
         d.barrier()
     del Cm
     torch.cuda.empty_cache()
-    return {"ms": ms, "rows": nr, "clocks": clk.summary(), "gather_ms": gather_ms,
-            "sample": sample}
+    return {"ms": ms, "compute_ms": compute_ms, "replicate_ms": rep_ms, "rows": nr,
+            "clocks": clk.summary(), "gather_ms": gather_ms, "sample": sample}
 
 
 def matmul_device_leg(steps: int, warmup: int) -> dict:
@@ -916,6 +979,9 @@ def run_b200(args) -> None:
         c4_tf32 = matmul_c4_leg(d, 2, 1, prec=1)
         c4_tf32["ms_max"] = d.max(c4_tf32["ms"])
         c4["ms_max"] = d.max(c4["ms"])
+        c4["compute_ms_max"] = d.max(c4["compute_ms"])
+        if c4["replicate_ms"] is not None:
+            c4["replicate_ms"] = d.max(c4["replicate_ms"])
         if c4["gather_ms"] is not None:
             c4["gather_ms"] = d.max(c4["gather_ms"])
     d.barrier()
@@ -1009,13 +1075,18 @@ def run_b200(args) -> None:
         flops = 2.0 * MM4 ** 3
         tf = flops / (c4["ms_max"] / 1e3) / 1e12
         per_gpu_flops = 2.0 * c4["rows"] * MM4 * MM4
-        ach = per_gpu_flops / (c4["ms"] / 1e3) / 1e12
+        ach = per_gpu_flops / (c4["compute_ms"] / 1e3) / 1e12
         peak = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
         line["matmul"] = {
-            "workload": "C4: MATMUL prec=bf16 (tcgen05), 32768^3, block rows of A/C per GPU, B replicated",
+            "workload": f"C4: MATMUL prec=bf16 (tcgen05), {MM4}^3, block rows of A/C per GPU, "
+                        "B replicated from per-GPU k-slices every step",
             "metric": "matmul TFLOP/s", "value": round(tf, 1), "unit": "TFLOP/s",
             "ms_per_step": round(c4["ms_max"], 3), "scaling": "strong",
-            "includes": "f32->bf16 operand preparation + GEMM + f32 C write",
+            "includes": ("f32->bf16 operand preparation + GEMM + f32 C write"
+                         + ("" if d.n == 1 else " + B all-gather (NCCL, side stream, pipelined under "
+                                                "the previous step's GEMM)")),
+            "compute_ms_per_step": round(c4["compute_ms_max"], 3),
+            "b_replicate_ms": None if c4["replicate_ms"] is None else round(c4["replicate_ms"], 3),
             "tolerance": "|c-c_ref| <= 1e-5 * sum|a||b| vs f64 oracle on bf16-rounded operands (tests/test_matmul_gpu.py)",
             "roofline": {"bound": "tensor", "kernel": "gemm::gemm2_kernel<bf16> (+ prep_a/prep_bt)",
                          "achieved": round(ach, 1),

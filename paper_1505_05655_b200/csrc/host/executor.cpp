@@ -195,7 +195,8 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     const obs::Range range("kernel");
     if (flag != Flag::LutApply) {
       if (G == 1) {
-        if (equalize && need_apply) {  // one fused launch: histogram -> LUT -> apply
+        if (need_apply) {  // one cooperative launch: statistics -> LUT -> apply
+          // (fused_kernel for equalize, stretch_fused_kernel for stretch)
           lut::launch_correct(dimg, dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr,
                               s.stream);
         } else if (equalize) {
@@ -230,8 +231,10 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
                                 cudaMemcpyDeviceToHost, s.stream));
     }
     if (need_apply) {
-      if (!(equalize && flag != Flag::LutApply))  // else applied by the fused launch
-        lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
+      // LUT_APPLY, and the multi-band stretch path, apply here; the other
+      // LUT_CORRECT paths applied inside their fused launch
+      const bool applied = flag != Flag::LutApply && (equalize || G == 1);
+      if (!applied) lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
       rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
       if (lut_out != nullptr && i == 0)
         GPCX_CUDA(cudaMemcpy(lut_out, s.d_lut(), task::kLutBytes, cudaMemcpyDeviceToHost));

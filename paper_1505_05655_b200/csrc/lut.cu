@@ -62,9 +62,13 @@ constexpr int kUnroll = 4;
 
 static_assert(kMaxParts * 8 <= 4 * 1024, "min/max slot area");
 
+// Streaming image load.  Coherent (no .nc): the LUT kernels may write their
+// output over their input (in == out) within the same launch, and PTX
+// defines .nc loads only on memory that is read-only for the whole kernel.
+// L1::no_allocate keeps the stream out of L1 like the .nc path did.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
@@ -278,8 +282,8 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
     for (int k = 0; k < 8; ++k) {
       const std::uint64_t p =
           static_cast<std::uint64_t>(static_cast<double>(threadIdx.x + 32 * k) * step);
-      a[k] = __ldg(img + p);
-      b[k] = __ldg(img + p + 1);
+      a[k] = __ldcg(img + p);
+      b[k] = __ldcg(img + p + 1);
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
