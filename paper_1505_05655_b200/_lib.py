@@ -7,10 +7,14 @@ usable, every compute call fails with GPCX_E_TASK_FAILED (-> GpcxError).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import sys
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgpcx.so"
+# GPCX_LIB_PATH selects another build of the same library (the
+# ThreadSanitizer build, tools/tsan_server.sh); the default is the product.
+LIB_PATH = Path(os.environ.get("GPCX_LIB_PATH") or
+                Path(__file__).resolve().parent / "lib" / "libgpcx.so")
 
 OK = 0
 ERRC_NAMES = [

@@ -108,11 +108,43 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+TSAN_LIB = LIB_DIR / "tsan" / "libgpcx.so"
+
+
+def build_tsan(verbose: bool = False) -> Path:
+    """ThreadSanitizer build of the host side (server pipeline, runtime,
+    registry, C ABI): the .cpp sources with -fsanitize=thread, linked with
+    the regular CUDA objects into lib/tsan/libgpcx.so.  Load it with
+    GPCX_LIB_PATH=<that file> and LD_PRELOAD=libtsan.so (tools/tsan_server.sh)."""
+    build()
+    out_dir = OBJ / "tsan"
+    out_dir.mkdir(parents=True, exist_ok=True)
+    TSAN_LIB.parent.mkdir(parents=True, exist_ok=True)
+    flags = [f for f in CXX_FLAGS if f not in ("-O2",)] + ["-O1", "-fsanitize=thread"]
+    jobs, objs = [], []
+    for rel in CPP_SOURCES:
+        obj = out_dir / (rel.replace("/", "_") + ".o")
+        objs.append(obj)
+        jobs.append((["g++", *flags, "-c", str(CSRC / rel), "-o", str(obj)], None))
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(lambda j: _run(*j), jobs))
+    cu_objs = [OBJ / (rel.replace("/", "_") + ".o") for rel in CU_SOURCES]
+    _run(["g++", "-shared", "-fsanitize=thread", "-o", str(TSAN_LIB), *map(str, objs),
+          *map(str, cu_objs), f"-L{CUDA_HOME / 'lib64'}", "-lcudart", "-lpthread",
+          f"-Wl,-rpath,{CUDA_HOME / 'lib64'}"])
+    if verbose:
+        print(f"built {TSAN_LIB}")
+    return TSAN_LIB
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--tsan", action="store_true", help="also build lib/tsan/libgpcx.so")
     args = ap.parse_args()
     build(force=args.force, verbose=True)
+    if args.tsan:
+        build_tsan(verbose=True)
 
 
 if __name__ == "__main__":
