@@ -1019,7 +1019,7 @@ def run_b200(args) -> None:
     gather = None
     if gather_ms is not None:
         gather = {"ms": round(gather_ms, 3), "bytes": 2 * ROWS * COLS,
-                  "what": "corrected bands gathered to rank 0 (torch.distributed.gather, "
+                  "what": "corrected bands gathered to rank 0 (exact-size point-to-point receives into the full image, shard.gather_bands; "
                           + ("gloo via host: GPCX_BENCH_ONE_GPU test mode" if Dist.one_gpu else "NCCL")
                           + "); not in `value` -- the output stays sharded in HBM there"}
     launches = 1 if exch_ms is None else 2

@@ -330,8 +330,12 @@ PinnedPool& pinned_pool() {
   static PinnedPool* p = new PinnedPool();
   return *p;
 }
-constexpr std::uint64_t kPinnedIdleCap = 8ull << 30;
 std::atomic<std::uint64_t> g_pinned_in_use{0};
+// Page-locked bytes leased at once (GPCX_PINNED_CAP_MB, default 32 GiB).
+// Idle pooled buffers are kept up to the same bound: freeing and
+// re-registering page-locked memory costs ~ms per GiB (cudaFreeHost /
+// cudaHostAlloc serialise with the whole context), so a server whose
+// in-flight staging exceeds a smaller idle cap churns on every request.
 std::uint64_t pinned_cap() {
   static const std::uint64_t cap = [] {
     const char* v = std::getenv("GPCX_PINNED_CAP_MB");
@@ -365,7 +369,7 @@ PinnedLease::~PinnedLease() {
   g_pinned_in_use.fetch_sub(cap_);
   PinnedPool& pool = pinned_pool();
   std::lock_guard<std::mutex> lock(pool.mu);
-  if (pool.idle_bytes + cap_ > kPinnedIdleCap) {
+  if (pool.idle_bytes + cap_ > pinned_cap()) {
     cudaFreeHost(ptr_);
   } else {
     pool.idle.emplace_back(cap_, ptr_);
