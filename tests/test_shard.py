@@ -165,3 +165,54 @@ def test_sharded_matmul_over_gloo_equals_single_process(world, m, k, n):
     A = O.synth_matrix(O.MAT_UNIFORM32, 9, m, k)
     B = O.synth_matrix(O.MAT_UNIFORM32, O.seed_b(9), k, n)
     assert got == O.matmul_f32(A, B).tobytes()
+
+
+def _mm_gpu_worker(rank, world, port, m, k, n, prec, q):
+    sys.path.insert(0, str(ROOT))
+    from paper_1505_05655_b200 import device as D
+    from paper_1505_05655_b200.shard import ShardedMatmul
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r0, nr = band(m, world, rank)
+    k0, nk = band(k, world, rank)
+    a = D.synth_matrix(1, 21, m, k, r0, nr)
+    b = D.synth_matrix(1, 22, k, n, k0, nk)
+
+    def mm(A, B):
+        C = torch.empty(A.shape[0], n, device="cuda")
+        D.matmul(prec, A, B, C, D.matmul_workspace(prec, A.shape[0], n, k))
+        return C
+
+    c = ShardedMatmul(dist, mm).run(a, b, k, n, world)
+    full = gather_bands(dist, c.cpu(), [nr_ for _, nr_ in bands(m, world)], n)
+    if rank == 0:
+        q.put(full.numpy().tobytes())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [0, 2])  # f32 SIMT, bf16 tcgen05
+@pytest.mark.parametrize("world,m,k,n", [(2, 1024, 768, 512), (3, 1000, 777, 520)])
+def test_sharded_matmul_device_path_bitwise_invariant(gpu, prec, world, m, k, n):
+    """The one-process-per-GPU MATMUL path with the sm_100a kernels: world
+    2 / 3 processes on cuda:0 (gloo for the plumbing), block rows of A / C,
+    B replicated from per-rank k-slices, C gathered -- bitwise equal to the
+    single-device product (acceptance.cpp:278-315's invariance, carried to
+    ranks)."""
+    from paper_1505_05655_b200 import device as D
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mm_gpu_worker, args=(r, world, port, m, k, n, prec, q))
+             for r in range(world)]
+    [p.start() for p in procs]
+    got = q.get(timeout=240)
+    [p.join(timeout=120) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    A = D.synth_matrix(1, 21, m, k)
+    B = D.synth_matrix(1, 22, k, n)
+    C = torch.empty(m, n, device="cuda")
+    D.matmul(prec, A, B, C, D.matmul_workspace(prec, m, n, k))
+    assert got == C.cpu().numpy().tobytes()

@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
     else if (MODE == 3) { if (slot & 1) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 4) { if ((slot & 3) == 3) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 5) redg(mine + v, 1);
+    else if (MODE == 12) { if ((slot & 15) == 15) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
+    else if (MODE == 13) { if ((slot & 31) == 31) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 7) reds(bins, v >> 2, 1u << ((v & 3) << 3));
     else if (MODE == 8) reds(bins + ((threadIdx.x >> 5) & 1) * 16384, v >> 2, 1u << ((v & 3) << 3));
     else if (MODE == 9) reds(bins + ((threadIdx.x >> 5) % 3) * 16384, v >> 2, 1u << ((v & 3) << 3));
@@ -84,9 +86,11 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
       if ((peers & ((1u << lane) - 1)) == 0) reds(bins, v >> 1, inc * __popc(peers));
     }
   };
+  uint32_t vslot = 0;  // 8 pixels per vector; modes 12/13 pick every 16th / 32nd
   auto vec = [&](uint4 q) {
-    px(q.x & 0xFFFF, 0); px(q.x >> 16, 1); px(q.y & 0xFFFF, 2); px(q.y >> 16, 3);
-    px(q.z & 0xFFFF, 4); px(q.z >> 16, 5); px(q.w & 0xFFFF, 6); px(q.w >> 16, 7);
+    const int b = (MODE == 12 || MODE == 13) ? (int)((vslot++ & 3) * 8) : 0;
+    px(q.x & 0xFFFF, b + 0); px(q.x >> 16, b + 1); px(q.y & 0xFFFF, b + 2); px(q.y >> 16, b + 3);
+    px(q.z & 0xFFFF, b + 4); px(q.z >> 16, b + 5); px(q.w & 0xFFFF, b + 6); px(q.w >> 16, b + 7);
   };
   uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
   for (; i + 3 * stride < nvec; i += 4 * stride) {
@@ -150,6 +154,8 @@ int main() {
     run<9>("9 red.shared u8 x3 replicas", img, n, parts, gh, sms);
     run<10>("10 atom u16 packed + ovf check", img, n, parts, gh, sms);
     run<11>("11 atom u8 x2 + ovf check", img, n, parts, gh, sms);
+    run<12>("12 1/16 red.global (additive)", img, n, parts, gh, sms);
+    run<13>("13 1/32 red.global (additive)", img, n, parts, gh, sms);
   }
   return 0;
 }
