@@ -61,13 +61,15 @@ std::string peer_name(int fd) {
   return std::string(text) + ":" + std::to_string(ntohs(sa.sin_port));
 }
 
-Conn::Conn(Fd fd, std::chrono::milliseconds idle) : fd_(std::move(fd)), idle_(idle) {
+Conn::Conn(Fd fd, std::chrono::milliseconds read_idle, std::chrono::milliseconds write_idle)
+    : fd_(std::move(fd)), read_idle_(read_idle), write_idle_(write_idle) {
   peer_ = peer_name(fd_.get());
 }
 
 void Conn::wait(short events) {
   pollfd p{fd_.get(), events, 0};
-  const int budget = idle_.count() < 0 ? -1 : static_cast<int>(idle_.count());
+  const auto idle = events == POLLIN ? read_idle_ : write_idle_;
+  const int budget = idle.count() < 0 ? -1 : static_cast<int>(idle.count());
   for (;;) {
     const int r = ::poll(&p, 1, budget);
     if (r > 0) return;  // ready, or an error / hangup the next syscall reports

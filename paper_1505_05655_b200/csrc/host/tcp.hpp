@@ -8,9 +8,11 @@
 // budget.  The wire contract is the reference's (proj/include/gpc/net.hpp:
 // 16-62): an idle peer surfaces as TimedOut, an orderly close before the
 // expected bytes as a zero read (-> Truncated in wire::read_exact).  Unlike
-// the reference, writes are bounded by the same idle budget (a client that
-// stops reading its response cannot pin a send thread forever) and the
-// listen backlog is SOMAXCONN, not 64 (proj/src/net.cpp:128).
+// the reference, writes are bounded too, by their own longer stall budget
+// (the server uses max(idle, 60 s)): a client that stops reading its
+// response cannot pin a send thread forever, while one that merely pauses
+// is not cut off at the read idle timeout.  The listen backlog is
+// SOMAXCONN, not 64 (proj/src/net.cpp:128).
 #pragma once
 
 #include <chrono>
@@ -48,27 +50,29 @@ class Fd {
   int fd_ = -1;
 };
 
-// One connected stream socket (non-blocking underneath).  `idle` bounds how
-// long a single read or write may wait for the peer; negative = forever.
+// One connected stream socket (non-blocking underneath).  `read_idle` /
+// `write_idle` bound how long a single read / write may wait for the peer;
+// negative = forever.
 class Conn : public wire::ByteStream {
  public:
   Conn() = default;
-  explicit Conn(Fd fd, std::chrono::milliseconds idle = std::chrono::milliseconds(-1));
+  explicit Conn(Fd fd, std::chrono::milliseconds read_idle = std::chrono::milliseconds(-1),
+                std::chrono::milliseconds write_idle = std::chrono::milliseconds(-1));
   std::size_t read_some(std::span<std::uint8_t> out) override;  // 0 = peer closed
   void write_all(std::span<const std::uint8_t> data) override;
   // Non-blocking read attempt: bytes read, 0 on orderly close, -1 when
   // nothing is available yet.  Errors throw IoError.
   long try_read(std::span<std::uint8_t> out);
-  void set_idle(std::chrono::milliseconds idle) { idle_ = idle; }
+
   int fd() const { return fd_.get(); }
   const std::string& peer() const { return peer_; }
   void close() { fd_.reset(); }
 
  private:
-  void wait(short events);  // TimedOut after idle_
+  void wait(short events);  // TimedOut after the direction's budget
   Fd fd_;
   std::string peer_;
-  std::chrono::milliseconds idle_{-1};
+  std::chrono::milliseconds read_idle_{-1}, write_idle_{-1};
 };
 
 // Blocking-semantics client connect (ConnectFailed); `host` is a name or
