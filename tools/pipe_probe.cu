@@ -38,11 +38,11 @@ __device__ __forceinline__ void st(uint4* p, uint4 v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-__device__ __forceinline__ void cnt(uint32_t* bins, uint32_t v, uint32_t* ovf) {
-  const uint32_t inc = 1u << ((v & 1) << 4);
-  const uint32_t old = atomicAdd(bins + (v >> 1), inc);
-  const uint32_t mask = (v & 1) ? 0xFFFF0000u : 0xFFFFu;
-  if ((old & mask) == mask) atomicAdd(ovf + v, 65536u);
+// red.shared on packed u16 pairs: the product's count rate (~0.48 ms per
+// 2^30 samples, tools/hist_probe mode 0) without its wrap bookkeeping
+__device__ __forceinline__ void cnt(uint32_t* bins, uint32_t v, uint32_t*) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(bins + (v >> 1));
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(1u << ((v & 1) << 4)) : "memory");
 }
 
 // count pass: grid-stride over the image, per-CTA packed u16 histogram,
@@ -143,7 +143,7 @@ int main() {
   });
   printf("count alone %.4f ms | apply alone %.4f ms | back to back %.4f ms per image (6 B/px: %.0f GB/s)\n", tc, ta,
          tca, 6.0 * n / tca / 1e6);
-  for (int x : {56, 64, 70, 74, 80, 88, 96}) {
+  for (int x : {64, 74, 84, 94, 104, 114, 124, 134}) {
     // per image: count(i+1) on x SMs || apply(i) on sms-x SMs; a barrier
     // per image pair (events) models the LUT dependency
     cudaEvent_t ec, ea;
