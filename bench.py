@@ -752,6 +752,56 @@ def c1_run(port: int, img: bytes, reps: int, warmup: int = 2) -> dict:
                 dtype=np.uint64))}
 
 
+def served_leg(n_gpus: int, reps: int = 5, matmul: bool = True) -> dict:
+    """The over-cap configs through the SERVED path (SURVEY.md §8d option ii):
+    header-only requests (synth=..., no payload) from the native client over
+    loopback TCP to the B200 server with all N GPUs bound.  C3: LUT_CORRECT
+    of the 32768^2 ramp12 scene generated on the GPUs, answered with the
+    corrected image's digest (checked against the oracle by the caller);
+    C4: MATMUL 32768^3 bf16, answered with 4096 seeded samples of C.  Per
+    request: generation (2 B/px / 8 B per matrix element written) + the task
+    + an 8-byte / 48 KiB response; median of `reps` after one warm-up."""
+    import struct
+    import paper_1505_05655_b200 as G
+    from paper_1505_05655_b200.client import submit_native as submit
+    G.init(bound_devices(n_gpus))
+    res = {}
+    try:
+        with G.Server(max_tasks=0) as srv:
+            params = f"rows={ROWS},cols={COLS},mode=equalize,synth=ramp12,seed={SEED}"
+            ts, digest = [], None
+            for i in range(reps + 1):
+                t = time.perf_counter()
+                r = submit("127.0.0.1", srv.port, "LUT_CORRECT", params, [], resp_cap=8,
+                           output_name="c3.digest")
+                assert r.ok, r.status
+                if i:
+                    ts.append(time.perf_counter() - t)
+                digest = struct.unpack("<Q", bytes(r.payload))[0]
+            ms = statistics.median(ts) * 1e3
+            res["c3"] = {"request": f"LUT_CORRECT {params} (no payload)", "ms_per_request": round(ms, 3),
+                         "value": round(ROWS * COLS / ms / 1e6, 2), "unit": "Gpixel/s",
+                         "includes": "scene generation on the GPUs (2 B/px written) + LUT_CORRECT + digest",
+                         "digest": digest}
+            if matmul:
+                mparams = f"m={MM4},k={MM4},n={MM4},prec=bf16,synth=uniform32,seed={SEED}"
+                ts = []
+                for i in range(3):
+                    t = time.perf_counter()
+                    r = submit("127.0.0.1", srv.port, "MATMUL", mparams, [], resp_cap=4096 * 12,
+                               output_name="c4.samples")
+                    assert r.ok, r.status
+                    if i:
+                        ts.append(time.perf_counter() - t)
+                ms = statistics.median(ts) * 1e3
+                res["c4"] = {"request": f"MATMUL {mparams} (no payload)", "ms_per_request": round(ms, 3),
+                             "value": round(2.0 * MM4 ** 3 / ms / 1e9, 1), "unit": "TFLOP/s",
+                             "includes": "A / B generation on the GPUs + operand prep + GEMM + 4096 samples"}
+    finally:
+        G.init([0])
+    return res
+
+
 def c1_leg(n_gpus: int) -> dict:
     import paper_1505_05655_b200 as G
     imgs, _ = c5_inputs(count=1)
@@ -1066,11 +1116,12 @@ def run_b200(args) -> None:
                                       "ms_per_step": round(e2e1["ms_per_step"], 2)},
                    "path": "gpcx_lut_host (C ABI), pinned host buffers, all N GPUs in-process; "
                            "each step = one full C3 scene in (2 GiB H2D) and out (2 GiB D2H)"}
-    c5 = c1 = None
+    c5 = c1 = served = None
     if args.workload in ("all", "c5"):
         time.sleep(2)  # let the clock recover from the C4 leg
         c5 = c5_leg(d.n)
         c1 = c1_leg(d.n)
+        served = served_leg(d.n, matmul=args.workload == "all")
     if c4 is not None:
         flops = 2.0 * MM4 ** 3
         tf = flops / (c4["ms_max"] / 1e3) / 1e12
@@ -1142,13 +1193,13 @@ def run_b200(args) -> None:
     # the TCP-bound C5 leg if they run before it
     # parity of the timed outputs (equalize and stretch) against the oracle
     # on the whole scene; at N=1 the same oracle runs are the CPU baseline
-    ref = cpu_lut_full(reps=3 if d.n == 1 else 1)
-    line["parity"] = {"equalize": lut_parity(lut, ref[0]), "stretch": lut_parity(stretch, ref[1])}
+    lut_ref = cpu_lut_full(reps=3 if d.n == 1 else 1)
+    line["parity"] = {"equalize": lut_parity(lut, lut_ref[0]), "stretch": lut_parity(stretch, lut_ref[1])}
     line["parity"]["ok"] = line["parity"]["equalize"]["ok"] and line["parity"]["stretch"]["ok"]
     line["stretch"]["parity"] = line["parity"]["stretch"]["ok"]
     if d.n == 1:
-        line["cpu_baseline"] = cpu_lut(ref, mode)
-        line["stretch"]["cpu_baseline"] = cpu_lut(ref, 1)
+        line["cpu_baseline"] = cpu_lut(lut_ref, mode)
+        line["stretch"]["cpu_baseline"] = cpu_lut(lut_ref, 1)
         if mm is not None:
             line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
         if dm is not None:
@@ -1166,6 +1217,11 @@ def run_b200(args) -> None:
             c1["output_identical_to_reference_server"] = ref.pop("digest") == c1["digest"]
         c1.pop("digest")
         line["c1"] = c1
+    if served is not None:
+        served["c3"]["parity"] = served["c3"].pop("digest") == lut_ref[0]["digest"]
+        served["workload"] = ("C3 / C4 through the B200 server as header-only requests (synth=, SURVEY 8d "
+                              "option ii): inputs generated on the GPUs, native client, loopback TCP")
+        line["served"] = served
     print(json.dumps(line), flush=True)
 
 

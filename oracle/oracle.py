@@ -92,6 +92,16 @@ def synth_matrix(kind: int, seed: int, rows: int, cols: int, row0: int = 0, nrow
     return out
 
 
+def splitmix64(x: int) -> int:
+    """The generators' hash, in Python: sample positions of
+    header-only MATMUL requests."""
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
 def seed_b(seed: int) -> int:
     return orc.orc_seed_b(seed)
 

@@ -102,7 +102,9 @@ void for_each_band(std::size_t count, Fn&& fn) {
 // LUT (GEN); `lut_out` optionally receives the LUT of CORRECT.
 gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t* img_in,
                         const std::uint16_t* lut_in, std::uint16_t* out_px,
-                        std::uint16_t* lut_out) {
+                        std::uint16_t* lut_out, const task::SynthParams* synth,
+                        std::uint64_t* digest_out) {
+  const bool synth_on = synth != nullptr && synth->on;
   const InflightGuard inflight;
   const std::uint64_t n = p.pixels();
   const auto* img = reinterpret_cast<const std::uint8_t*>(img_in);
@@ -143,7 +145,11 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     const Band& b = bands[i];
     const std::uint64_t bn = b.nrows * p.cols;
     s.a.ensure(bn * 2);
-    rt::h2d(s, s.a.ptr, img + b.row0 * p.cols * 2, bn * 2);
+    if (synth_on)  // the band's rows, generated in place (header-only request)
+      synth::launch_image(synth->kind, synth->seed, p.rows, p.cols, b.row0, b.nrows,
+                          s.a.as<std::uint16_t>(), s.stream);
+    else
+      rt::h2d(s, s.a.ptr, img + b.row0 * p.cols * 2, bn * 2);
     if (flag == Flag::LutApply) {
       rt::h2d(s, s.d_lut(), lut_in, task::kLutBytes);
       return;
@@ -186,6 +192,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
 
   // Phase 2: LUT on every device, apply, DMA each band into its slice.
   std::vector<gpcx_lut_stats> stats(G);
+  std::vector<std::uint64_t> digests(G, 0);
   for_each_band(G, [&](std::size_t i) {
     rt::Slot& s = *leases[i];
     rt::use_device(s.device);
@@ -235,7 +242,15 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       // LUT_CORRECT paths applied inside their fused launch
       const bool applied = flag != Flag::LutApply && (equalize || G == 1);
       if (!applied) lut::launch_apply(s.d_lut(), dimg, dimg, bn, s.stream);
-      rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
+      if (synth_on) {  // the band's share of the position-keyed digest
+        GPCX_CUDA(cudaMemsetAsync(s.d_digest(), 0, 8, s.stream));
+        synth::launch_digest(dimg, bn, b.row0 * p.cols, s.d_digest(), s.stream);
+        GPCX_CUDA(cudaMemcpyAsync(s.h_digest(), s.d_digest(), 8, cudaMemcpyDeviceToHost, s.stream));
+        GPCX_CUDA(cudaStreamSynchronize(s.stream));
+        digests[i] = *s.h_digest();
+      } else {
+        rt::d2h(s, outb + b.row0 * p.cols * 2, dimg, bn * 2);
+      }
       if (lut_out != nullptr && i == 0)
         GPCX_CUDA(cudaMemcpy(lut_out, s.d_lut(), task::kLutBytes, cudaMemcpyDeviceToHost));
     } else if (i == 0) {
@@ -246,11 +261,32 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
     if (flag != Flag::LutApply) stats[i] = *s.h_stats();
   });
 
+  if (digest_out != nullptr) {
+    std::uint64_t sum = 0;  // mod 2^64: the digest is additive over bands
+    for (const std::uint64_t d : digests) sum += d;
+    *digest_out = sum;
+  }
   return flag == Flag::LutApply ? gpcx_lut_stats{n, 0, 0, 0} : stats[0];
 }
 
-void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* Cout) {
+namespace {
+
+// Sample positions of a synthetic MATMUL (task_spec.hpp).
+std::vector<uint2> synth_positions(const task::MatmulParams& p, const task::SynthParams& sy) {
+  std::vector<uint2> pos(sy.samples);
+  for (std::uint64_t j = 0; j < sy.samples; ++j)
+    pos[j] = make_uint2(static_cast<std::uint32_t>(synth::splitmix64_host(sy.seed ^ (2 * j)) % p.m),
+                        static_cast<std::uint32_t>(synth::splitmix64_host(sy.seed ^ (2 * j + 1)) % p.n));
+  return pos;
+}
+
+// Block-row MATMUL over the planned devices.  Host operands (A, B, C), or
+// with `sy` on: A's rows and B's k-slices generated on the devices and the
+// sampled entries of C written to `samples_out`.
+void matmul_run(const task::MatmulParams& p, const float* A, const float* B, float* Cout,
+                const task::SynthParams* sy, std::uint8_t* samples_out) {
   const InflightGuard inflight;
+  const bool synth_on = sy != nullptr && sy->on;
   auto* outb = reinterpret_cast<std::uint8_t*>(Cout);
   const std::vector<Band> bands = plan_bands(p.m, 2 * p.m * p.n * p.k, kShardMinFlops);
   const std::size_t G = bands.size();
@@ -265,6 +301,7 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
   std::vector<std::uint64_t> ks(G + 1, 0);
   for (std::size_t i = 0; i <= G; ++i) ks[i] = std::min<std::uint64_t>(p.k, (p.k + G - 1) / G * i);
   const std::uint64_t row_bytes = p.n * 4;
+  const std::vector<uint2> positions = synth_on ? synth_positions(p, *sy) : std::vector<uint2>();
 
   for_each_band(G, [&](std::size_t i) {
     rt::Slot& s = *leases[i];
@@ -273,12 +310,20 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
     s.a.ensure(std::max<std::uint64_t>(b.nrows * p.k * 4, 4));
     s.b.ensure(std::max<std::uint64_t>(p.k * row_bytes, 4));
     s.c.ensure(std::max<std::uint64_t>(b.nrows * p.n * 4, 4));
-    // A before B: a request payload (A || B) may still be arriving
-    // (rt::Arrival), and A lands first.
-    rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
-    rt::h2d(s, s.b.as<std::uint8_t>() + ks[i] * row_bytes,
-            reinterpret_cast<const std::uint8_t*>(B) + ks[i] * row_bytes,
-            (ks[i + 1] - ks[i]) * row_bytes);
+    if (synth_on) {  // generated in place: A (seed), B (splitmix64(seed))
+      synth::launch_matrix(sy->kind, sy->seed, p.m, p.k, b.row0, b.nrows, s.a.as<float>(), s.stream);
+      synth::launch_matrix(sy->kind, synth::splitmix64_host(sy->seed), p.k, p.n, ks[i],
+                           ks[i + 1] - ks[i],
+                           reinterpret_cast<float*>(s.b.as<std::uint8_t>() + ks[i] * row_bytes),
+                           s.stream);
+    } else {
+      // A before B: a request payload (A || B) may still be arriving
+      // (rt::Arrival), and A lands first.
+      rt::h2d(s, s.a.ptr, A + b.row0 * p.k, b.nrows * p.k * 4);
+      rt::h2d(s, s.b.as<std::uint8_t>() + ks[i] * row_bytes,
+              reinterpret_cast<const std::uint8_t*>(B) + ks[i] * row_bytes,
+              (ks[i + 1] - ks[i]) * row_bytes);
+    }
     GPCX_CUDA(cudaEventRecord(s.ready, s.stream));
   });
 
@@ -309,8 +354,51 @@ void matmul_host(const task::MatmulParams& p, const float* A, const float* B, fl
     // A peer may still be reading this device's B slice; every band's d2h
     // synchronises its own stream, and for_each_band joins them all before
     // any slot (and its B) returns to the pool.
-    rt::d2h(s, outb + b.row0 * p.n * 4, s.c.ptr, b.nrows * p.n * 4);
+    if (!synth_on) {
+      rt::d2h(s, outb + b.row0 * p.n * 4, s.c.ptr, b.nrows * p.n * 4);
+      return;
+    }
+    // the samples in this band's rows: positions up, gathered values down,
+    // in chunks through the slot's 256 KiB histogram scratch
+    std::vector<std::uint64_t> mine;
+    for (std::uint64_t j = 0; j < positions.size(); ++j)
+      if (positions[j].x >= b.row0 && positions[j].x < b.row0 + b.nrows) mine.push_back(j);
+    constexpr std::uint64_t kChunk = 16384;  // 16384 x (8 + 4) B < 256 KiB
+    rt::PinnedLease host = rt::pinned_acquire(kChunk * 12);
+    auto* hpos = static_cast<uint2*>(host.get());
+    auto* hval = reinterpret_cast<float*>(hpos + kChunk);
+    auto* dpos = reinterpret_cast<uint2*>(s.d_hist());
+    auto* dval = reinterpret_cast<float*>(dpos + kChunk);
+    for (std::uint64_t c0 = 0; c0 < mine.size(); c0 += kChunk) {
+      const std::uint64_t cn = std::min<std::uint64_t>(kChunk, mine.size() - c0);
+      for (std::uint64_t q = 0; q < cn; ++q) {
+        const uint2 rc = positions[mine[c0 + q]];
+        hpos[q] = make_uint2(rc.x - static_cast<std::uint32_t>(b.row0), rc.y);
+      }
+      GPCX_CUDA(cudaMemcpyAsync(dpos, hpos, cn * 8, cudaMemcpyHostToDevice, s.stream));
+      synth::launch_gather(s.c.as<float>(), p.n, dpos, static_cast<std::uint32_t>(cn), dval, s.stream);
+      GPCX_CUDA(cudaMemcpyAsync(hval, dval, cn * 4, cudaMemcpyDeviceToHost, s.stream));
+      GPCX_CUDA(cudaStreamSynchronize(s.stream));
+      for (std::uint64_t q = 0; q < cn; ++q) {
+        const std::uint64_t j = mine[c0 + q];
+        std::uint8_t* e = samples_out + j * task::kSynthSampleBytes;
+        std::memcpy(e, &positions[j].x, 4);
+        std::memcpy(e + 4, &positions[j].y, 4);
+        std::memcpy(e + 8, &hval[q], 4);
+      }
+    }
+    GPCX_CUDA(cudaStreamSynchronize(s.stream));
   });
+}
+
+}  // namespace
+
+void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* Cout) {
+  matmul_run(p, A, B, Cout, nullptr, nullptr);
+}
+
+void matmul_synth(const task::MatmulParams& p, const task::SynthParams& sy, std::uint8_t* out) {
+  matmul_run(p, nullptr, nullptr, nullptr, &sy, out);
 }
 
 void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
@@ -458,20 +546,41 @@ wire::ParamMap execute_admitted(Flag flag, const wire::ParamMap& params,
                                  " bytes, need " + std::to_string(want_out));
   if (flag == Flag::Matmul) {
     const task::MatmulParams p = task::parse_matmul(params);
-    const auto* A = reinterpret_cast<const float*>(in.data());
-    matmul_host(p, A, A + p.m * p.k, reinterpret_cast<float*>(out.data()));
+    const task::SynthParams sy = task::parse_synth(flag, params);
+    if (sy.on) {
+      matmul_synth(p, sy, out.data());
+    } else {
+      const auto* A = reinterpret_cast<const float*>(in.data());
+      matmul_host(p, A, A + p.m * p.k, reinterpret_cast<float*>(out.data()));
+    }
     result.set("m", p.m);
     result.set("n", p.n);
     result.set("k", p.k);
     result.set("prec", task::prec_name(p.prec));
+    if (sy.on) {
+      result.set("synth", params.get("synth"));
+      result.set("seed", sy.seed);
+      result.set("samples", sy.samples);
+    }
     return result;
   }
   const task::LutParams p = task::parse_lut(flag, params);
   const auto* words = reinterpret_cast<const std::uint16_t*>(in.data());
   const bool apply_only = flag == Flag::LutApply;
-  const gpcx_lut_stats st = lut_host(flag, p, apply_only ? words + 65536 : words,
-                                     apply_only ? words : nullptr,
-                                     reinterpret_cast<std::uint16_t*>(out.data()), nullptr);
+  const task::SynthParams sy = apply_only ? task::SynthParams{} : task::parse_synth(flag, params);
+  gpcx_lut_stats st;
+  if (sy.on) {  // header-only: the image is generated on the devices
+    std::uint64_t digest = 0;
+    const bool correct = flag == Flag::LutCorrect;
+    st = lut_host(flag, p, nullptr, nullptr,
+                  correct ? nullptr : reinterpret_cast<std::uint16_t*>(out.data()), nullptr, &sy,
+                  correct ? &digest : nullptr);
+    if (correct)
+      for (int b = 0; b < 8; ++b) out[b] = static_cast<std::uint8_t>(digest >> (8 * b));
+  } else {
+    st = lut_host(flag, p, apply_only ? words + 65536 : words, apply_only ? words : nullptr,
+                  reinterpret_cast<std::uint16_t*>(out.data()), nullptr);
+  }
   result.set("rows", p.rows);
   result.set("cols", p.cols);
   if (!apply_only) {
@@ -479,6 +588,10 @@ wire::ParamMap execute_admitted(Flag flag, const wire::ParamMap& params,
     result.set("lo", static_cast<std::uint64_t>(st.lo));
     result.set("hi", static_cast<std::uint64_t>(st.hi));
     if (p.mode == GPCX_LUT_EQUALIZE) result.set("cdf_min", st.cdf_min);
+  }
+  if (sy.on) {
+    result.set("synth", params.get("synth"));
+    result.set("seed", sy.seed);
   }
   return result;
 }

@@ -26,10 +26,17 @@ wire::ParamMap execute_admitted(task::Flag flag, const wire::ParamMap& params,
 
 // The same, on typed host buffers and without the wire's 1 GiB cap (the
 // in-process entry points gpcx_lut_host / gpcx_matmul_host).
+// With `synth` on, the image is generated on the devices (img == nullptr)
+// and LUT_CORRECT returns the corrected image's position-keyed digest in
+// *digest instead of the pixels (out == nullptr).
 gpcx_lut_stats lut_host(task::Flag flag, const task::LutParams& p, const std::uint16_t* img,
                         const std::uint16_t* lut_in, std::uint16_t* out,
-                        std::uint16_t* lut_out);
+                        std::uint16_t* lut_out, const task::SynthParams* synth = nullptr,
+                        std::uint64_t* digest = nullptr);
 void matmul_host(const task::MatmulParams& p, const float* A, const float* B, float* C);
+// A synthetic MATMUL: A / B generated on the devices, `samples` entries of
+// C written to `out` as (u32 row, u32 col, f32 value) LE (task_spec.hpp).
+void matmul_synth(const task::MatmulParams& p, const task::SynthParams& synth, std::uint8_t* out);
 // BAYER_BILINEAR / BAYER_GRADIENT on host buffers (out: 3 planes).
 void bayer_host(bool gradient, const task::BayerParams& p, const std::uint16_t* in,
                 std::uint16_t* out);

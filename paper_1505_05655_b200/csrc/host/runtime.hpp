@@ -70,6 +70,13 @@ struct Slot {
                                              65536 * 4);
   }
   gpcx_lut_stats* h_stats() const { return static_cast<gpcx_lut_stats*>(h_small.ptr); }
+  // u64 digest scratch next to the stats (device) / in the readback buffer
+  std::uint64_t* d_digest() const {
+    return reinterpret_cast<std::uint64_t*>(small.as<unsigned char>() + 131072 + 128);
+  }
+  std::uint64_t* h_digest() const {
+    return reinterpret_cast<std::uint64_t*>(static_cast<unsigned char*>(h_small.ptr) + 128);
+  }
   ~Slot();
 };
 

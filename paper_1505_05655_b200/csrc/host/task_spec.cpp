@@ -71,11 +71,53 @@ const char* phase_name(int phase) {
   return kNames[phase & 3];
 }
 
+namespace {
+// Dimension check of a synthetic request: nothing crosses the wire, so the
+// bound is the kernels' (fewer than 2^32 elements), not the 1 GiB cap.
+std::uint64_t synth_elems(std::string_view a_key, std::uint64_t a, std::string_view b_key,
+                          std::uint64_t b) {
+  if (a == 0 || b == 0)
+    fail(Errc::BadValue, std::string(a == 0 ? a_key : b_key) + " must be positive");
+  if (a >= (1ull << 32) || b >= (1ull << 32) || a * b >= (1ull << 32))
+    fail(Errc::Overflow, std::string(a_key) + "*" + std::string(b_key) +
+                             " must stay below 2^32 elements");
+  return a * b;
+}
+}  // namespace
+
+SynthParams parse_synth(Flag f, const wire::ParamMap& params) {
+  SynthParams s;
+  if (!params.has("synth")) return s;
+  const std::string kind = params.get("synth");
+  s.on = true;
+  if (f == Flag::LutGen || f == Flag::LutCorrect) {
+    if (kind == "ramp12") s.kind = GPCX_IMG_RAMP12;
+    else if (kind == "uniform16") s.kind = GPCX_IMG_UNIFORM16;
+    else fail(Errc::BadValue, "synth=" + kind);
+  } else if (f == Flag::Matmul) {
+    if (kind == "exact8") s.kind = GPCX_MAT_EXACT8;
+    else if (kind == "uniform32") s.kind = GPCX_MAT_UNIFORM32;
+    else fail(Errc::BadValue, "synth=" + kind);
+    if (params.has("samples")) s.samples = params.get_uint("samples");
+    if (s.samples == 0 || s.samples > (1ull << 20))
+      fail(Errc::BadValue, "samples must be 1 .. 1048576");
+  } else {
+    fail(Errc::BadValue, std::string("synth= is not supported by ") + flag_name(f));
+  }
+  if (params.has("seed")) s.seed = params.get_uint("seed");
+  return s;
+}
+
 LutParams parse_lut(Flag f, const wire::ParamMap& params) {
   LutParams p;
   p.rows = params.get_uint("rows");
   p.cols = params.get_uint("cols");
-  wire::dim_product("rows", p.rows, "cols", p.cols, 2);  // validates + caps
+  if (params.has("synth") && f == Flag::LutApply)
+    fail(Errc::BadValue, "synth= is not supported by LUT_APPLY (its LUT is an input)");
+  if (params.has("synth"))
+    synth_elems("rows", p.rows, "cols", p.cols);
+  else
+    wire::dim_product("rows", p.rows, "cols", p.cols, 2);  // validates + caps
   const std::string dtype = params.get_or("dtype", "u16");
   if (dtype != "u16") fail(Errc::BadValue, "dtype=" + dtype);
   if (f != Flag::LutApply) {
@@ -92,10 +134,16 @@ MatmulParams parse_matmul(const wire::ParamMap& params) {
   p.m = params.get_uint("m");
   p.k = params.get_uint("k");
   p.n = params.get_uint("n");
-  const std::uint64_t a_bytes = wire::dim_product("m", p.m, "k", p.k, 4);
-  const std::uint64_t b_bytes = wire::dim_product("k", p.k, "n", p.n, 4);
-  wire::capped_sum(a_bytes, b_bytes);
-  wire::dim_product("m", p.m, "n", p.n, 4);  // the response must fit too
+  if (params.has("synth")) {
+    synth_elems("m", p.m, "k", p.k);
+    synth_elems("k", p.k, "n", p.n);
+    synth_elems("m", p.m, "n", p.n);
+  } else {
+    const std::uint64_t a_bytes = wire::dim_product("m", p.m, "k", p.k, 4);
+    const std::uint64_t b_bytes = wire::dim_product("k", p.k, "n", p.n, 4);
+    wire::capped_sum(a_bytes, b_bytes);
+    wire::dim_product("m", p.m, "n", p.n, 4);  // the response must fit too
+  }
   const std::string prec = params.get_or("prec", "f32");
   if (prec == "f32") p.prec = GPCX_PREC_F32;
   else if (prec == "tf32") p.prec = GPCX_PREC_TF32;
@@ -127,7 +175,7 @@ std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
     case Flag::LutGen:
     case Flag::LutCorrect: {
       const LutParams p = parse_lut(f, params);
-      return p.pixels() * 2;
+      return parse_synth(f, params).on ? 0 : p.pixels() * 2;
     }
     case Flag::LutApply: {
       const LutParams p = parse_lut(f, params);
@@ -135,7 +183,7 @@ std::uint64_t payload_len(Flag f, const wire::ParamMap& params) {
     }
     case Flag::Matmul: {
       const MatmulParams p = parse_matmul(params);
-      return (p.m * p.k + p.k * p.n) * 4;
+      return parse_synth(f, params).on ? 0 : (p.m * p.k + p.k * p.n) * 4;
     }
     case Flag::BayerBilinear:
     case Flag::BayerGradient: {
@@ -169,11 +217,15 @@ std::uint64_t output_len(Flag f, const wire::ParamMap& params) {
       parse_lut(f, params);
       return kLutBytes;
     case Flag::LutApply:
-    case Flag::LutCorrect:
       return parse_lut(f, params).pixels() * 2;
+    case Flag::LutCorrect: {
+      const LutParams p = parse_lut(f, params);
+      return parse_synth(f, params).on ? 8 : p.pixels() * 2;
+    }
     case Flag::Matmul: {
       const MatmulParams p = parse_matmul(params);
-      return p.m * p.n * 4;
+      const SynthParams s = parse_synth(f, params);
+      return s.on ? s.samples * kSynthSampleBytes : p.m * p.n * 4;
     }
     case Flag::BayerBilinear:
     case Flag::BayerGradient: {

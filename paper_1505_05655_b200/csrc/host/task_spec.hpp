@@ -17,6 +17,22 @@
 // prec=f32|tf32|bf16 (MATMUL); dtype=u16, phase=RGGB|BGGR|GRBG|GBRG
 // (BAYER_*, as proj/src/tasks.cpp:13-35).  Sizes follow the reference's
 // dim_product() rules and the 1 GiB kMaxPayload cap.
+//
+// Header-only synthetic requests (SURVEY.md §8d option ii): with
+// synth=ramp12|uniform16 (LUT_GEN, LUT_CORRECT) or synth=exact8|uniform32
+// (MATMUL) and optional seed=S (default 24301 = 0x5eed) the request carries
+// NO payload (marker 0x00): the inputs are generated on the GPUs by the
+// counter-based generators (the same bits the oracle generates), so the
+// over-cap configs C3 / C4 run through the served path.  The 1 GiB cap then
+// bounds only the response:
+//   LUT_GEN     -> the LUT (131072 B), rows*cols < 2^32
+//   LUT_CORRECT -> 8 bytes: the position-keyed u64 digest of the corrected
+//                  image, sum_i splitmix64((i << 16) | out[i]) mod 2^64
+//   MATMUL      -> samples=N (default 4096, <= 2^20) entries of C, each
+//                  (u32 row, u32 col, f32 value) LE; entry j is at
+//                  row = splitmix64(seed ^ 2j) mod m, col = splitmix64(seed ^
+//                  (2j+1)) mod n; A uses seed, B splitmix64(seed); m*k, k*n and
+//                  m*n < 2^32 elements each.
 #pragma once
 
 #include <cstdint>
@@ -56,6 +72,14 @@ struct BayerParams {
   int phase = 0;  // gpc::img::CfaPhase ordinal: RGGB, BGGR, GRBG, GBRG
 };
 
+struct SynthParams {
+  bool on = false;
+  int kind = 0;  // GPCX_IMG_* (LUT) or GPCX_MAT_* (MATMUL)
+  std::uint64_t seed = 0x5EED;
+  std::uint64_t samples = 4096;  // MATMUL only
+};
+inline constexpr std::uint64_t kSynthSampleBytes = 12;  // u32 row, u32 col, f32 value
+
 struct LsqParams {
   std::uint64_t lines = 0, pixels = 0;
   int order = 0;
@@ -68,6 +92,8 @@ LutParams parse_lut(Flag f, const wire::ParamMap& params);
 // order (OrderTooHigh above 8), dtype.
 LsqParams parse_lsq(const wire::ParamMap& params);
 MatmulParams parse_matmul(const wire::ParamMap& params);
+// synth= / seed= / samples= (BadValue for a flag or kind that has none).
+SynthParams parse_synth(Flag f, const wire::ParamMap& params);
 BayerParams parse_bayer(const wire::ParamMap& params);
 
 std::uint64_t payload_len(Flag f, const wire::ParamMap& params);

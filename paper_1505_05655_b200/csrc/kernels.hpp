@@ -136,6 +136,12 @@ void launch_matrix(int kind, std::uint64_t seed, std::uint64_t rows,
 void launch_digest(const std::uint16_t* v, std::uint64_t n,
                    std::uint64_t index0, std::uint64_t* digest,
                    cudaStream_t stream);
+// out[j] = c[rc[j].row * ldc + rc[j].col] for `count` (u32 row, u32 col)
+// pairs in device memory (sampled entries of a synthetic MATMUL).
+void launch_gather(const float* c, std::uint64_t ldc, const void* rc, std::uint32_t count,
+                   float* out, cudaStream_t stream);
+// The generators' hash, on the host (seeds, sample positions).
+std::uint64_t splitmix64_host(std::uint64_t x);
 // A kernel that executes __trap() (gpcx_debug_fault: a real sticky error).
 void launch_trap(cudaStream_t stream);
 }  // namespace synth
