@@ -206,6 +206,9 @@ def test_digest_matches_oracle(gpu):
     img = D.synth_image(O.IMG_UNIFORM16, 5, 777, 1001)
     d = D.digest_u16(img, 12345)
     assert int(d.item()) & (2 ** 64 - 1) == O.digest_u16(u16(img), 12345)
+    for off in (1, 3, 7, 8):  # unaligned starts: scalar head, 128-bit body, tail
+        d = D.digest_u16(img[off:], off)
+        assert int(d.item()) & (2 ** 64 - 1) == O.digest_u16(u16(img)[off:], off), off
 
 
 @pytest.mark.slow
