@@ -48,7 +48,8 @@
 extern "C" {
 #endif
 
-#define GPCX_ABI_VERSION 1
+/* 2: gpcx_server_stats gained busy / dropped; health, debug-fault and synth= requests */
+#define GPCX_ABI_VERSION 2
 
 /* 0 = OK; n > 0 = 1 + gpc::Errc ordinal (proj/include/gpc/error.hpp:11-46). */
 typedef enum gpcx_status {
@@ -116,7 +117,9 @@ int gpcx_device_count(int* count); /* devices bound (after init) */
  * address, launch failure / trap, ...): no request is routed to it any
  * more and sharded requests use the remaining devices; with none left GPU
  * tasks answer ERR:TASK_FAILED.  `why` (may be NULL) receives the error
- * that caused the quarantine.  Rebinding with gpcx_init resets the state. */
+ * that caused the quarantine.  Rebinding with gpcx_init resets the state.
+ * (The reference has no device state: its failure boundary is the handler
+ * exception -> ERR:TASK_FAILED, proj/src/registry.cpp:113-118.) */
 int gpcx_device_health(int index, int* healthy, char* why, uint64_t why_cap);
 /* Test hook for the health machinery: kind 0 quarantines bound index
  * `index` without touching the GPU; kind 1 launches a kernel that traps on

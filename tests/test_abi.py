@@ -29,7 +29,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version_and_flags():
-    assert G.lib.gpcx_abi_version() == 1
+    assert G.lib.gpcx_abi_version() == 2
     assert G.flags() == ["BAYER_BILINEAR", "BAYER_GRADIENT", "DEVINFO", "LSQ_POLYFIT", "LUT_APPLY",
                          "LUT_CORRECT", "LUT_GEN", "MATMUL"]
     assert G.required_params("LSQ_POLYFIT") == ["lines", "pixels", "order"]
