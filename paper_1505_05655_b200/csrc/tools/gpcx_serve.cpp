@@ -8,7 +8,7 @@
 // GPUs bound with --devices (default: every visible device).
 //
 //   gpcx-serve [--bind 0.0.0.0] [--port 5555] [--max-tasks N] [--timeout S]
-//              [--devices 0,1,...]
+//              [--max-pending N] [--devices 0,1,...]
 //
 // Talks only to the C ABI (include/gpcx.h).
 #include <pthread.h>
@@ -29,7 +29,7 @@ constexpr int kExitOk = 0, kExitUsage = 2, kExitFailed = 1;
 void usage(const char* argv0) {
   std::fprintf(stderr,
                "usage: %s [--bind ADDR] [--port N] [--max-tasks N] [--timeout SECONDS]\n"
-               "          [--devices 0,1,...]\n",
+               "          [--max-pending N] [--devices 0,1,...]\n",
                argv0);
 }
 
@@ -67,6 +67,10 @@ int main(int argc, char** argv) {
       max_tasks = n;
     } else if (a == "--timeout" && parse_int(v, 1, 86400, &n)) {
       timeout_secs = n;
+    } else if (a == "--max-pending" && parse_int(v, 1, 1 << 20, &n)) {
+      // admission control of the staged server (include/gpcx.h): read from
+      // the environment when the server starts
+      setenv("GPCX_MAX_PENDING", v, 1);
     } else if (a == "--devices") {
       for (const char* p = v; *p != '\0';) {
         char* end = nullptr;
@@ -118,6 +122,11 @@ int main(int argc, char** argv) {
   int sig = 0;
   sigwait(&signals, &sig);
   std::fprintf(stderr, "signal %d, draining\n", sig);
+  gpcx_server_stats st{};
+  if (gpcx_server_stats_get(server, &st) == 0)
+    std::fprintf(stderr, "served %llu requests (busy %llu, dropped %llu)\n",
+                 static_cast<unsigned long long>(st.requests), static_cast<unsigned long long>(st.busy),
+                 static_cast<unsigned long long>(st.dropped));
   const int rc = gpcx_server_stop(server);
   gpcx_shutdown();
   return rc == 0 ? kExitOk : kExitFailed;
