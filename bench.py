@@ -998,13 +998,22 @@ def traffic_from_profiles() -> dict:
 
 def run_b200(args) -> None:
     import torch
+    leg_s: dict[str, float] = {}
+
+    def _leg(name, fn, *a, **k):
+        """Runs one leg, adding its wall-clock seconds to `bench_legs_s`."""
+        t = time.perf_counter()
+        try:
+            return fn(*a, **k)
+        finally:
+            leg_s[name] = round(leg_s.get(name, 0.0) + time.perf_counter() - t, 2)
     d = Dist(args.gpus)
     d.init("nccl")
     mode = 0
-    lut = lut_device_leg(d, args.steps, args.warmup, mode)
+    lut = _leg("lut_device_leg", lut_device_leg, d, args.steps, args.warmup, mode)
     # the other LUT mode (contrast stretch): min/max instead of a histogram
     # at N=1 (read-only reduction, no atomics); the same exchange at N>1
-    stretch = lut_device_leg(d, args.steps, args.warmup, 1, gather=False)
+    stretch = _leg("lut_device_leg", lut_device_leg, d, args.steps, args.warmup, 1, gather=False)
     stretch_ms = d.max(stretch["ms"])
     ms = d.max(lut["ms"])
     exch_ms = d.max(lut["exch_ms"]) if lut["exch_ms"] is not None else None
@@ -1015,18 +1024,18 @@ def run_b200(args) -> None:
     dm = None
     if args.workload in ("all", "demosaic") and d.rank == 0:
         torch.cuda.empty_cache()
-        dm = demosaic_leg(max(3, min(args.steps, 10)), 3)
+        dm = _leg("demosaic_leg", demosaic_leg, max(3, min(args.steps, 10)), 3)
     mm = c4 = c4_tf32 = None
     if args.workload in ("all", "matmul"):
         torch.cuda.empty_cache()
         # C2 before C4: right after the 1 kW C4 GEMMs the power controller
         # still holds the clock down for a while
         if d.rank == 0:
-            mm = matmul_device_leg(max(3, min(args.steps, 10)), 2)
+            mm = _leg("matmul_device_leg", matmul_device_leg, max(3, min(args.steps, 10)), 2)
         d.barrier()
-        c4 = matmul_c4_leg(d, max(2, min(args.steps, 5)), 1)
+        c4 = _leg("matmul_c4_leg", matmul_c4_leg, d, max(2, min(args.steps, 5)), 1)
         # the TF32 tensor-core path on the same C4 problem (kind::tf32)
-        c4_tf32 = matmul_c4_leg(d, 2, 1, prec=1)
+        c4_tf32 = _leg("matmul_c4_leg", matmul_c4_leg, d, 2, 1, prec=1)
         c4_tf32["ms_max"] = d.max(c4_tf32["ms"])
         c4["ms_max"] = d.max(c4["ms"])
         c4["compute_ms_max"] = d.max(c4["compute_ms"])
@@ -1105,8 +1114,8 @@ def run_b200(args) -> None:
     # with 2 in flight the pipeline fill / drain (first H2D, last D2H alone)
     # is amortised over K like any other part of the job
     e2e_steps = max(4, args.steps)
-    e2e1 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=1)
-    e2e2 = lut_e2e_leg(d.n, e2e_steps, 1, mode, inflight=2)
+    e2e1 = _leg("lut_e2e_leg", lut_e2e_leg, d.n, e2e_steps, 1, mode, inflight=1)
+    e2e2 = _leg("lut_e2e_leg", lut_e2e_leg, d.n, e2e_steps, 1, mode, inflight=2)
     best = e2e2 if e2e2["value"] > e2e1["value"] else e2e1
     line["e2e"] = {"value": round(best["value"], 3), "unit": "Gpixel/s",
                    "h2d_bytes_per_step": best["h2d_bytes_per_step"],
@@ -1119,9 +1128,9 @@ def run_b200(args) -> None:
     c5 = c1 = served = None
     if args.workload in ("all", "c5"):
         time.sleep(2)  # let the clock recover from the C4 leg
-        c5 = c5_leg(d.n)
-        c1 = c1_leg(d.n)
-        served = served_leg(d.n, matmul=args.workload == "all")
+        c5 = _leg("c5_leg", c5_leg, d.n)
+        c1 = _leg("c1_leg", c1_leg, d.n)
+        served = _leg("served_leg", served_leg, d.n, matmul=args.workload == "all")
     if c4 is not None:
         flops = 2.0 * MM4 ** 3
         tf = flops / (c4["ms_max"] / 1e3) / 1e12
@@ -1169,7 +1178,7 @@ def run_b200(args) -> None:
                                 "achieved": round(mm["tflops"], 2), "peak": 74.4,
                                 "frac": round(mm["tflops"] / 74.4, 4)},
                    "l2": "flushed between steps (256 MiB write)", "clocks": mm["clocks"]}
-        mm_line["e2e"] = matmul_e2e_leg(3)
+        mm_line["e2e"] = _leg("matmul_e2e_leg", matmul_e2e_leg, 3)
         line.setdefault("matmul", {})["c2_f32"] = mm_line
     if dm is not None:
         kern = {}
@@ -1188,12 +1197,12 @@ def run_b200(args) -> None:
                          "frac": kern["bilinear"]["frac"], "traffic": tr.get("demosaic_kernel", {}).get("bytes_per_launch")},
             "kernels": kern, "l2": "inputs + outputs (2 GiB) larger than L2",
             "parity": "byte-identical to the reference's img::demosaic_* and gpcref oracles (tests/test_demosaic.py)"}
-        line["demosaic"]["e2e"] = demosaic_task_leg()
+        line["demosaic"]["e2e"] = _leg("demosaic_task_leg", demosaic_task_leg)
     # CPU baselines last: their all-core OpenMP runs heat the host and slow
     # the TCP-bound C5 leg if they run before it
     # parity of the timed outputs (equalize and stretch) against the oracle
     # on the whole scene; at N=1 the same oracle runs are the CPU baseline
-    lut_ref = cpu_lut_full(reps=3 if d.n == 1 else 1)
+    lut_ref = _leg("cpu_lut_full", cpu_lut_full, reps=3 if d.n == 1 else 1)
     line["parity"] = {"equalize": lut_parity(lut, lut_ref[0]), "stretch": lut_parity(stretch, lut_ref[1])}
     line["parity"]["ok"] = line["parity"]["equalize"]["ok"] and line["parity"]["stretch"]["ok"]
     line["stretch"]["parity"] = line["parity"]["stretch"]["ok"]
@@ -1201,18 +1210,18 @@ def run_b200(args) -> None:
         line["cpu_baseline"] = cpu_lut(lut_ref, mode)
         line["stretch"]["cpu_baseline"] = cpu_lut(lut_ref, 1)
         if mm is not None:
-            line["matmul"]["c2_f32"]["cpu_baseline"] = cpu_matmul()
+            line["matmul"]["c2_f32"]["cpu_baseline"] = _leg("cpu_matmul", cpu_matmul)
         if dm is not None:
-            line["demosaic"]["cpu_baseline"] = cpu_demosaic()
+            line["demosaic"]["cpu_baseline"] = _leg("cpu_demosaic", cpu_demosaic)
         if c4 is not None and c4.get("sample") is not None:
-            line["matmul"]["cpu_baseline"] = cpu_matmul_c4(c4["sample"])
+            line["matmul"]["cpu_baseline"] = _leg("cpu_matmul_c4", cpu_matmul_c4, c4["sample"])
     if c5 is not None:
         if d.n == 1:
-            c5["cpu_baseline"] = cpu_c5()
+            c5["cpu_baseline"] = _leg("cpu_c5", cpu_c5)
         line["c5"] = c5
     if c1 is not None:
         if d.n == 1:
-            ref = cpu_c1()
+            ref = _leg("cpu_c1", cpu_c1)
             c1["cpu_baseline"] = ref
             c1["output_identical_to_reference_server"] = ref.pop("digest") == c1["digest"]
         c1.pop("digest")
@@ -1222,6 +1231,7 @@ def run_b200(args) -> None:
         served["workload"] = ("C3 / C4 through the B200 server as header-only requests (synth=, SURVEY 8d "
                               "option ii): inputs generated on the GPUs, native client, loopback TCP")
         line["served"] = served
+    line["bench_legs_s"] = leg_s
     print(json.dumps(line), flush=True)
 
 
