@@ -392,3 +392,40 @@ def test_dropped_connections_are_counted(server):
         assert c.recv(16) == b""  # dropped at the 300 ms idle timeout, no response
     time.sleep(0.1)
     assert server.stats()["dropped"] >= before + 1
+
+
+def test_stop_drains_admitted_requests(refl):
+    """Server.stop() first stops accepting, then lets every admitted request
+    finish: a request whose payload is still arriving when stop() is called
+    is received, run and answered before stop() returns."""
+    s = G.Server(max_tasks=2, idle_timeout_ms=5000).start()
+    c = socket.create_connection(("127.0.0.1", s.port), timeout=30)
+    c.sendall(W.header("LUT_CORRECT", "rows=64,cols=64", has_payload=True) + b"\0" * 1000)
+    time.sleep(0.3)  # admitted, receiving
+    stopper = threading.Thread(target=s.stop)
+    stopper.start()
+    time.sleep(0.3)
+    assert stopper.is_alive()  # waiting for the in-flight request
+    c.sendall(b"\0" * (8192 - 1000))
+    resp = W.parse_response(c.recv(4096))
+    assert resp["status"].startswith(("OK", "ERR:TASK_FAILED"))  # TASK_FAILED without a GPU
+    stopper.join(timeout=30)
+    assert not stopper.is_alive()
+    c.close()
+    with pytest.raises(OSError):  # no longer listening
+        socket.create_connection(("127.0.0.1", s.port), timeout=2).close()
+
+
+def test_synth_request_is_header_only(server):
+    """A header-only synthetic request (synth=, no payload, marker 0x00) is
+    admitted without reading a payload byte; a payload marker on it is a
+    PAYLOAD_MISMATCH, like any task whose rule says 0 bytes."""
+    resp = W.parse_response(W.roundtrip(server.port, W.header(
+        "LUT_CORRECT", "rows=32768,cols=32768,synth=ramp12", name="d.bin")))
+    # OK with a GPU (8-byte digest), TASK_FAILED without one -- never a read
+    assert resp["status"] in ("OK", "ERR:TASK_FAILED") and resp["name"] == "d.bin"
+    if resp["status"] == "OK":
+        assert len(resp["payload"]) == 8
+    with socket.create_connection(("127.0.0.1", server.port), timeout=30) as c:
+        c.sendall(W.header("LUT_CORRECT", "rows=4,cols=4,synth=ramp12", has_payload=True))
+        assert W.parse_response(c.recv(4096))["status"] == "ERR:PAYLOAD_MISMATCH"
