@@ -234,6 +234,43 @@ def test_c3_full_size_via_digest(gpu, mode, mname, kind):
     assert int(D.digest_u16(out).item()) & (2 ** 64 - 1) == O.digest_u16(r_out)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("mode,mname", MODES)
+@pytest.mark.parametrize("pattern", ["flat", "binary", "sparse"])
+def test_c3_full_size_degenerate_images(gpu, mode, mname, pattern):
+    """The C3 size (2^30 pixels) on the images that stress the count pass's
+    special paths hardest: one value everywhere (every CTA's bin wraps its
+    u16 half-word ~110 times; the warp-combining path), two values (the
+    binary path) and 8 values spread over the range.  Expected LUT / stats
+    from the oracle on the exact u64 histogram; out == LUT[in] everywhere."""
+    torch, D = _dev()
+    rows = cols = 32768
+    n = rows * cols
+    hist = np.zeros(65536, dtype=np.uint64)
+    if pattern == "flat":
+        img = torch.full((n,), 12345, dtype=torch.int16, device="cuda")
+        hist[12345] = n
+    elif pattern == "binary":
+        img = torch.full((n,), 1000, dtype=torch.int16, device="cuda")
+        img[n // 3:] = 30000
+        hist[1000], hist[30000] = n // 3, n - n // 3
+    else:
+        vals = torch.tensor([7, 4095, 4096, 20000, 32767, 100, 2, 31000], dtype=torch.int16, device="cuda")
+        img = vals.repeat(n // 8)
+        for v in vals.tolist():
+            hist[v] = n // 8
+    out = torch.empty_like(img)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    D.lut_correct(img, out, mode, lut, stats, ws)
+    r_lut, r_st = O.lut_from_hist(hist, mode)
+    assert np.array_equal(u16(lut), r_lut)
+    assert D.read_stats(stats) == r_st
+    lut_t = torch.from_numpy(r_lut.astype(np.int32)).cuda()
+    for a, b in zip(img.split(1 << 28), out.split(1 << 28)):
+        want = lut_t[a.to(torch.int32) & 0xFFFF].to(torch.int16)
+        assert torch.equal(b, want)
+
+
 # ----------------------------------------------------------- task level ---
 
 @pytest.mark.parametrize("mode,mname", MODES)

@@ -13,6 +13,14 @@
 //   8 / 9  u8 quads, 2 / 3 replicas (warp w uses replica w % R)
 //   10 atom (returning) u16 pairs + the wrap check (the product's count_one)
 //   11 atom u8 quads x2 replicas + wrap check
+//   12 / 13  1/16 / 1/32 of the pixels to red.global (an additive L2 channel
+//            next to the product's smem atomics -- VERDICT r1 item 4)
+//   14 LANE-PRIVATE window: bins [900, 900 + 3584) as u16 pairs, lane L's
+//      copy interleaved so word ((v - 900) >> 1) * 32 + L sits in bank L
+//      (conflict-free by construction); atom + wrap check; values outside
+//      the window to red.global (224 KiB of smem)
+//   15 the same with u8 quads (window of 7168 values), wrap check per byte
+//   16 mode 14 with red (no return, no wrap check): its upper bound
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -53,7 +61,8 @@ template <int MODE>
 __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh) {
   extern __shared__ uint4 sm[];
   uint32_t* bins = (uint32_t*)sm;
-  for (int i = threadIdx.x; i < (MODE == 9 ? 12288 : 8192); i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
+  constexpr int kZero = MODE == 9 ? 12288 : (MODE >= 14 ? 14336 : 8192);
+  for (int i = threadIdx.x; i < kZero; i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* mine = gh + (uint64_t)blockIdx.x * 65536;
@@ -67,6 +76,25 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
     else if (MODE == 3) { if (slot & 1) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 4) { if ((slot & 3) == 3) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 5) redg(mine + v, 1);
+    else if (MODE == 14 || MODE == 16) {
+      const uint32_t d = v - 900u;
+      if (d < 3584u) {
+        const uint32_t w = (d >> 1) * 32u + lane, in = 1u << ((d & 1) << 4);
+        if (MODE == 16) reds(bins, w, in);
+        else {
+          const uint32_t old = atomicAdd(bins + w, in);
+          const uint32_t mask = (d & 1) ? 0xFFFF0000u : 0xFFFFu;
+          if ((old & mask) == mask) redg(mine + v, 65536);
+        }
+      } else redg(mine + v, 1);
+    } else if (MODE == 15) {
+      const uint32_t d = v - 900u;
+      if (d < 7168u) {
+        const uint32_t sh = (d & 3) << 3;
+        const uint32_t old = atomicAdd(bins + (d >> 2) * 32u + lane, 1u << sh);
+        if (((old >> sh) & 0xFFu) == 0xFFu) redg(mine + v, 256);
+      } else redg(mine + v, 1);
+    }
     else if (MODE == 12) { if ((slot & 15) == 15) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 13) { if ((slot & 31) == 31) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 7) reds(bins, v >> 2, 1u << ((v & 3) << 3));
@@ -108,7 +136,7 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
 
 template <int MODE>
 void run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh, int sms) {
-  const int smem = MODE == 9 ? 3 * 65536 : 131072;
+  const int smem = MODE == 9 ? 3 * 65536 : (MODE >= 14 ? 14336 * 16 : 131072);
   cudaFuncSetAttribute(hist<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -156,6 +184,9 @@ int main() {
     run<11>("11 atom u8 x2 + ovf check", img, n, parts, gh, sms);
     run<12>("12 1/16 red.global (additive)", img, n, parts, gh, sms);
     run<13>("13 1/32 red.global (additive)", img, n, parts, gh, sms);
+    run<14>("14 lane-private u16 window", img, n, parts, gh, sms);
+    run<15>("15 lane-private u8 window", img, n, parts, gh, sms);
+    run<16>("16 lane-private u16, red only", img, n, parts, gh, sms);
   }
   return 0;
 }
