@@ -60,7 +60,11 @@ constexpr int kSmemHist = kWords * 4;  // 128 KiB
 constexpr int kSmemLut = kBins * 2;    // 128 KiB
 constexpr int kUnroll = 4;
 
-static_assert(kMaxParts * 8 <= 4 * 1024, "min/max slot area");
+// u32 work counter of the apply pass's dynamic tail (apply_image), in the
+// unused end of the min/max slot area; reset before the grid sync that
+// precedes every cooperative apply.
+constexpr std::uint64_t kTailOff = kMinMaxOff + 4 * 1024 - 64;
+static_assert(kMaxParts * 8 <= 4 * 1024 - 64, "min/max slot area");
 
 // Streaming image load.  Coherent (no .nc): the LUT kernels may write their
 // output over their input (in == out) within the same launch, and PTX
@@ -392,10 +396,17 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
 // out = LUT[in] over [0, n) with the LUT in smem; CTA `cta` of `ctas`.
 // Two vectors per stage, the next stage's loads in flight while this one is
 // looked up and stored (tools/apply_bench.cu: = cudaMemcpy D2D bandwidth).
+// With `tail` (cooperative launches, counter zeroed before their last grid
+// sync) the last 4 x ctas chunks of 8 vectors per thread are not assigned
+// statically but taken chunk by chunk from the counter: CTAs do not stream
+// at identical rates (the static split left a ~20 us spread between the
+// first and the last CTA to finish, profiles/r1/fused_trace_v2_c3.txt), and
+// the dynamic tail lets the early ones take the late ones' share.
 template <int kSwz>
 __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const std::uint16_t* in,
                                             std::uint16_t* out, std::uint64_t n, int cta,
-                                            int ctas) {
+                                            int ctas, std::uint32_t* tail = nullptr) {
+  constexpr std::uint64_t kChunk = 8ull * kThreads;  // vectors per tail chunk (128 KiB)
   const std::uint64_t tid = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
   const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
   const std::uint64_t head = head_len(in, n);
@@ -405,17 +416,20 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
   if (tid < n - tail0) out[tail0 + tid] = lut_at<kSwz>(s_lut, in[tail0 + tid]);
   const uint4* src = reinterpret_cast<const uint4*>(in + head);
   uint4* dst = reinterpret_cast<uint4*>(out + head);
+  const std::uint64_t tail_chunks = 4ull * static_cast<std::uint64_t>(ctas);
+  const bool dynamic = tail != nullptr && nvec >= 16 * tail_chunks * kChunk;
+  const std::uint64_t static_end = dynamic ? nvec - tail_chunks * kChunk : nvec;
   constexpr int kU = 2;
   std::uint64_t i = tid;
   uint4 q[kU], nq[kU];
-  bool have = i + (kU - 1) * stride < nvec;
+  bool have = i + (kU - 1) * stride < static_end;
   if (have) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) q[u] = ld_stream(src + i + u * stride);
   }
   while (have) {
     const std::uint64_t nx = i + kU * stride;
-    const bool nhave = nx + (kU - 1) * stride < nvec;
+    const bool nhave = nx + (kU - 1) * stride < static_end;
     if (nhave) {
 #pragma unroll
       for (int u = 0; u < kU; ++u) nq[u] = ld_stream(src + nx + u * stride);
@@ -427,7 +441,22 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
     i = nx;
     have = nhave;
   }
-  for (; i < nvec; i += stride) st_stream(dst + i, lookup_vec<kSwz>(s_lut, ld_stream(src + i)));
+  for (; i < static_end; i += stride) st_stream(dst + i, lookup_vec<kSwz>(s_lut, ld_stream(src + i)));
+  if (!dynamic) return;
+  __shared__ std::uint32_t s_chunk;
+  for (;;) {
+    __syncthreads();  // the previous chunk index is consumed
+    if (threadIdx.x == 0) s_chunk = atomicAdd(tail, 1u);
+    __syncthreads();
+    const std::uint64_t c = s_chunk;
+    if (c >= tail_chunks) break;
+    const std::uint64_t v0 = static_end + c * kChunk + threadIdx.x;
+    uint4 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = ld_stream(src + v0 + u * kThreads);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) st_stream(dst + v0 + u * kThreads, lookup_vec<kSwz>(s_lut, x[u]));
+  }
 }
 
 // floor(num / d) for num < 2^53 and d >= 1 without a 64-bit integer divide
@@ -581,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  uint32_t* __restrict__ hist, SliceSummary* __restrict__ blocks, int mode,
                  std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
                  int stages, const PeerTable* __restrict__ peers, std::uint32_t seq,
-                 unsigned long long timeout_ns) {
+                 unsigned long long timeout_ns, std::uint32_t* __restrict__ tail) {
   extern __shared__ uint4 smem_u4[];
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
   __shared__ unsigned long long s_wsum[8], s_wfcount[8];
@@ -796,6 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   LUT_STAMP(6);
   if (!(stages & kApply)) return;
+  if (blockIdx.x == 0 && t == 0) *tail = 0;  // apply's dynamic tail, published by the sync
   grid.sync();
   LUT_STAMP(7);
 
@@ -806,9 +836,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   else stage_lut<0>(smem_u4, lut);
   __syncthreads();
   LUT_STAMP(8);
-  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x);
-  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x);
-  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
 #ifdef GPCX_LUT_TRACE
   __syncthreads();
 #endif
@@ -964,7 +994,7 @@ __device__ __forceinline__ void build_stretch_lut(uint32_t* s_words, std::uint16
 __global__ void __launch_bounds__(kThreads, 1)
     stretch_fused_kernel(const std::uint16_t* img, std::uint16_t* out,  // may alias (in place)
                          std::uint64_t n, uint2* __restrict__ slots, std::uint16_t* lut_g,
-                         gpcx_lut_stats* stats) {
+                         gpcx_lut_stats* stats, std::uint32_t* __restrict__ tail) {
   extern __shared__ uint4 smem_u4[];
   __shared__ uint32_t smn[32], smx[32], s_swz;
   cg::grid_group grid = cg::this_grid();
@@ -1010,6 +1040,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mx = __reduce_max_sync(0xFFFFFFFFu, smx[lane]);
     if (lane == 0) slots[blockIdx.x] = make_uint2(mn, mx);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tail = 0;  // apply's dynamic tail
   grid.sync();
   if (warp == 0) {
     mn = 0xFFFFFFFFu;
@@ -1036,9 +1067,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   else build_stretch_lut<0>(s_words, lut_g, n, lo, hi);
   __syncthreads();
   const std::uint16_t* s_lut = reinterpret_cast<const std::uint16_t*>(smem_u4);
-  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x);
-  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x);
-  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x);
+  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
 }
 
 bool g_attrs_set[64] = {};
@@ -1085,12 +1116,13 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
   auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
   auto* blocks = reinterpret_cast<SliceSummary*>(base + kBlocksOff);
+  auto* tail = reinterpret_cast<std::uint32_t*>(base + kTailOff);
   if (hist == nullptr) hist = reinterpret_cast<uint32_t*>(base + kHistOff);
   const int sms = device_sm_count();
   int nparts = parts_for(n, sms);
   void* args[] = {const_cast<std::uint16_t**>(&img), &out, &n, &nparts, &parts, &overflow,
                   &hist, &blocks, &mode, &lut, &stats, &stages,
-                  const_cast<PeerTable**>(&peers), &seq, &timeout_ns};
+                  const_cast<PeerTable**>(&peers), &seq, &timeout_ns, &tail};
   GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fused_kernel),
                                         dim3(std::max(sms, kSlices)), dim3(kThreads), args,
                                         kSmemHist, stream));
@@ -1147,8 +1179,9 @@ void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n
   if (mode == GPCX_LUT_STRETCH && co_aligned(in, out) && n != 0 && stretch_fused_enabled()) {
     set_attrs_once();
     auto* slots = reinterpret_cast<uint2*>(static_cast<unsigned char*>(ws) + kMinMaxOff);
+    auto* tail = reinterpret_cast<std::uint32_t*>(static_cast<unsigned char*>(ws) + kTailOff);
     const int sms = device_sm_count();
-    void* args[] = {const_cast<std::uint16_t**>(&in), &out, &n, &slots, &lut, &stats};
+    void* args[] = {const_cast<std::uint16_t**>(&in), &out, &n, &slots, &lut, &stats, &tail};
     GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(stretch_fused_kernel),
                                           dim3(sms), dim3(kThreads), args, kSmemLut, stream));
     return;

@@ -5,6 +5,11 @@
 //   ./tools/fused_trace [rows cols]
 #include "../paper_1505_05655_b200/csrc/lut.cu"
 
+// the library's device-health hook (host/runtime.cpp) is not linked here
+namespace gpcx::rt {
+void note_cuda_error(cudaError_t, const char*) {}
+}  // namespace gpcx::rt
+
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
