@@ -604,6 +604,15 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
   return x;
 }
 
+// Warp sum of totals: one redux.sync when they are known to fit in 32 bits
+// (a single call's image, n < 2^32), the u64 shuffle tree only for a peer
+// group's summed histogram (`wide`).  The redux keeps phase 3 at its
+// round-1 length (~2.5 us vs ~5.8 us with the u64 tree, fused_trace).
+__device__ __forceinline__ unsigned long long warp_sum_total(unsigned long long x, bool wide) {
+  if (wide) return warp_sum_u64(x);
+  return __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(x));
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     fused_kernel(const std::uint16_t* img, std::uint16_t* out, std::uint64_t n, int nparts,
                  uint32_t* __restrict__ parts, uint32_t* __restrict__ overflow,
@@ -790,12 +799,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (tc.x != 0) hi = max(hi, fl.y);
     }
-    n64 = warp_sum_u64(n64);
-    off = warp_sum_u64(off);
+    const bool wide = stages & kExchange;  // peers' counts summed in: totals may exceed 2^32
+    n64 = warp_sum_total(n64, wide);
+    off = warp_sum_total(off, wide);
     const uint32_t my_lo = lo;
     lo = __reduce_min_sync(0xFFFFFFFFu, lo);
     hi = __reduce_max_sync(0xFFFFFFFFu, hi);
-    const unsigned long long cdf_min64 = warp_sum_u64(my_lo == lo ? lo_count : 0ull);
+    const unsigned long long cdf_min64 = warp_sum_total(my_lo == lo ? lo_count : 0ull, wide);
     unsigned long long warp_off = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
