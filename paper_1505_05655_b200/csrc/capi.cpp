@@ -247,7 +247,7 @@ void gpcx_pinned_free(void* ptr) {
 int gpcx_lut_workspace_size(uint64_t n, uint64_t* bytes) {
   return guarded([&] {
     need_u32(n);
-    *bytes = gpcx::lut::workspace_bytes();
+    *bytes = gpcx::lut::workspace_bytes(n);
   });
 }
 
@@ -328,7 +328,7 @@ int gpcx_lut_correct_device(const uint16_t* in, uint16_t* out, uint64_t n, int m
     need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
     if (mode != GPCX_LUT_EQUALIZE && mode != GPCX_LUT_STRETCH)
       gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
-    gpcx::lut::launch_correct(in, out, n, mode, lut, stats, ws, as_stream(stream));
+    gpcx::lut::launch_correct(in, out, n, mode, lut, stats, ws, as_stream(stream), ws_bytes);
   });
 }
 
@@ -376,7 +376,7 @@ int gpcx_lut_correct_peer_device(gpcx_lut_peer* p, const uint16_t* in, uint16_t*
       gpcx::fail(gpcx::Errc::BadValue, "mode " + std::to_string(mode));
     need_u32(n);
     need_ws(ws, ws_bytes, gpcx::lut::workspace_bytes());
-    p->rank.correct(in, out, n, mode, lut, stats, ws, as_stream(stream));
+    p->rank.correct(in, out, n, mode, lut, stats, ws, as_stream(stream), ws_bytes);
   });
 }
 

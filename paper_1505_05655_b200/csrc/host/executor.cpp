@@ -204,8 +204,10 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       if (G == 1) {
         if (need_apply) {  // one cooperative launch: statistics -> LUT -> apply
           // (fused_kernel for equalize, stretch_fused_kernel for stretch)
+          // (a workspace with room for the residual plane at scene sizes)
+          if (equalize) s.lut_ws.ensure(lut::workspace_bytes(bn), /*zero=*/true);
           lut::launch_correct(dimg, dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr,
-                              s.stream);
+                              s.stream, s.lut_ws.cap);
         } else if (equalize) {
           lut::launch_hist_lut(dimg, bn, p.mode, s.d_lut(), s.d_stats(), s.lut_ws.ptr, s.stream);
         } else {

@@ -77,12 +77,12 @@ void LutRank::connect(const cudaIpcMemHandle_t* handles) {
 
 void LutRank::correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
                       std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, std::uint64_t ws_bytes) {
   if (!connected_) fail(Errc::BadValue, "peer group not connected");
   GPCX_CUDA(cudaSetDevice(device_));
   const std::uint32_t seq = ++seq_;
   lut::launch_correct_peer(d_table_, hist_at(block_, seq & 1), seq, timeout_ns_, in, out, n,
-                           mode, lut, stats, ws, stream);
+                           mode, lut, stats, ws, stream, ws_bytes);
 }
 
 }  // namespace gpcx::peer

@@ -42,7 +42,8 @@ class LutRank {
   // One step of the group: every rank must make the same sequence of
   // calls (each call advances the shared sequence number).
   void correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
-               std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+               std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream,
+               std::uint64_t ws_bytes = 0);
 
   int rank() const { return rank_; }
   int nranks() const { return nranks_; }

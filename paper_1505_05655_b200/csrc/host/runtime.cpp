@@ -57,7 +57,11 @@ void DeviceBuf::ensure(std::uint64_t bytes, bool zero) {
   const std::uint64_t want = std::max<std::uint64_t>(bytes, 256);
   GPCX_CUDA(cudaMalloc(&ptr, want));
   cap = want;
-  if (zero) GPCX_CUDA(cudaMemset(ptr, 0, want));
+  if (zero) {
+    // complete before any (non-blocking) stream uses the buffer
+    GPCX_CUDA(cudaMemset(ptr, 0, want));
+    GPCX_CUDA(cudaStreamSynchronize(nullptr));
+  }
 }
 
 void DeviceBuf::release() {

@@ -24,7 +24,14 @@ inline constexpr int kMaxParts = 296;         // per-CTA partial histograms
 //   [256 Ki, 512 Ki)          merged histogram, u32[65536]
 //   [512 Ki, +kMaxParts*8)    per-CTA (lo, hi) pairs for the min/max path
 //   [.. , + kMaxParts*128 Ki) per-CTA packed partial histograms
+//   [workspace_bytes(), +plane_bytes(n))  the residual plane of an n-sample
+//                             LUT_CORRECT (lut.cu); absent below 2^25 samples
 std::uint64_t workspace_bytes();
+// Recommended size for n samples (fixed part + residual plane).  Launchers
+// given a workspace of at least this size code the plane; one of at least
+// workspace_bytes() is enough for every path.
+std::uint64_t workspace_bytes(std::uint64_t n);
+std::uint64_t plane_bytes(std::uint64_t n);
 // The merged-histogram scratch inside a workspace (u32[65536]).
 std::uint32_t* ws_hist(void* ws);
 
@@ -63,7 +70,7 @@ inline constexpr std::uint64_t kPeerBlockBytes = kPeerHistBytes + kPeerFlagBytes
 void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::uint32_t seq,
                          std::uint64_t timeout_ns, const std::uint16_t* in, std::uint16_t* out,
                          std::uint64_t n, int mode, std::uint16_t* lut, gpcx_lut_stats* stats,
-                         void* ws, cudaStream_t stream);
+                         void* ws, cudaStream_t stream, std::uint64_t ws_bytes = 0);
 // Host-ordered second half for the in-process planner: sum the group's
 // published histograms (table->flags unused), LUT, apply the band.
 void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mode,
@@ -90,7 +97,8 @@ void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::u
 // Single-device LUT_CORRECT (LUT_GEN + apply; in == out allowed): equalize
 // with co-aligned buffers is ONE fused_kernel launch; otherwise gen + apply.
 void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
-                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
+                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream,
+                    std::uint64_t ws_bytes = 0);
 void launch_minmax(const std::uint16_t* img, std::uint64_t n,
                    gpcx_lut_stats* stats, void* ws, cudaStream_t stream);
 void launch_from_minmax(const gpcx_lut_stats* stats, std::uint16_t* lut,

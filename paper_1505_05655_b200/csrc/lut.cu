@@ -271,12 +271,15 @@ __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, u
 //          binary or few-level images; noise-free ramps too) -> the count
 //          pass probes each warp's diversity and combines equal values.
 //          Ordinary images skip that probe (it costs ~2.5% on them).
+//   bit 3  smooth data: >= 1/2 of the pairs differ by < 64 -> worth coding
+//          the residual plane (fused_kernel); noise-like images skip its
+//          per-block test, which would mark every block raw (~3% on them).
 // Warp 0 computes the flags into *flags; the caller's next __syncthreads
 // publishes them.  They change where and how counts are added, never what.
 __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uint64_t n,
                                               uint32_t* flags) {
   if (threadIdx.x >= 32) return;
-  uint32_t o = 0, eq = 0;
+  uint32_t o = 0, eq = 0, near = 0;
   if (n >= 2) {
     // 8 pairs per lane, all 16 loads in flight at once (this runs while
     // the other warps zero the histogram, and C1's whole kernel is ~40 us)
@@ -293,16 +296,18 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
     for (int k = 0; k < 8; ++k) {
       o |= a[k] | b[k];
       eq += a[k] == b[k];
+      near += (a[k] > b[k] ? a[k] - b[k] : b[k] - a[k]) < 64u;
     }
   } else if (n == 1 && threadIdx.x == 0) {
     o = img[0];
   }
   o = __reduce_or_sync(0xFFFFFFFFu, o);
   eq = __reduce_add_sync(0xFFFFFFFFu, eq);
+  near = __reduce_add_sync(0xFFFFFFFFu, near);
   if (threadIdx.x == 0) {
     const uint32_t tz = o == 0 ? 32u : static_cast<uint32_t>(__ffs(o) - 1);
     const uint32_t layout = (n == 0 || tz < 3) ? 0u : (tz <= 6 ? 1u : 2u);
-    *flags = layout | (eq >= 32 ? 4u : 0u);
+    *flags = layout | (eq >= 32 ? 4u : 0u) | (near >= 128 ? 8u : 0u);
   }
 }
 
@@ -456,6 +461,259 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
     for (int u = 0; u < 8; ++u) x[u] = ld_stream(src + v0 + u * kThreads);
 #pragma unroll
     for (int u = 0; u < 8; ++u) st_stream(dst + v0 + u * kThreads, lookup_vec<kSwz>(s_lut, x[u]));
+  }
+}
+
+// ---- the residual plane: a narrow copy of the image, count -> apply ------
+// The count pass is bound by the shared-memory atomic unit (~0.47 ms at C3
+// against a 0.335 ms read floor: HBM idles ~30% of it), the apply pass by
+// HBM (2 B read + 2 B written per sample).  With room in the workspace
+// (workspace_bytes(n)), the count pass also stores every 512-sample block
+// (64 vectors: two adjacent 512-byte warp loads) whose samples lie in a
+// 256-value window as a base word and one residual byte per sample
+// (code_block); the apply pass reads that 1 B/px copy instead of the
+// 2 B/px image.  Bytes move from the HBM-bound pass into the atomic-bound
+// one: 2 + 1 (count) and 1 + 2 (apply) per sample instead of 2 and 2 + 2 --
+// the same 6 B/px, but no pass idles HBM.  Other blocks (noise-like data)
+// get base word kRawBlock and are applied from the image.
+// Exact by construction: v = base + residual.  Block b = vectors
+// [64b, 64b + 64) of the 16-byte-aligned body, lane l holding vectors
+// 64b + l and 64b + 32 + l (residuals: 16 bytes at plane vector 32b + l);
+// plane layout: u32 base[n >> 9] (256-byte rounded) | 512 bytes per block.
+constexpr uint32_t kRawBlock = 0x10000u;
+constexpr std::uint64_t kPlaneMin = 1ull << 25;  // samples; below it the image stays in L2
+
+__host__ __device__ __forceinline__ std::uint64_t plane_base_bytes(std::uint64_t n) {
+  return ((n >> 9) * 4 + 255) & ~std::uint64_t{255};
+}
+
+__device__ __forceinline__ uint4 ld_plane(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// One block (the warp's 64 vectors, all lanes active).  Base = lane 0's
+// first sample - 128 (clamped to [0, 65280]); the block is narrow when every
+// sample lies in [base, base + 255] -- tested on the plain 32-bit
+// differences q - base (per u16 half): a half outside the window leaves a
+// non-zero high byte in its half (an underflowing low half included, since
+// base <= 65280), and with none outside there is no borrow, so the low
+// bytes are the residuals.  One shuffle and one vote per block, no min/max
+// tree (the count pass is issue-sensitive: +35 instructions per block of a
+// redux min/max version cost ~75 us at C3).
+__device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk, uint32_t lane,
+                                           uint32_t* pbase, uint4* pres) {
+#if defined(GPCX_PLANE_PROBE) && GPCX_PLANE_PROBE == 2  // timing probe only (wrong results)
+  const uint32_t f = q0.x & 0xFFFFu;
+#else
+  const uint32_t f = __shfl_sync(0xFFFFFFFFu, q0.x, 0) & 0xFFFFu;
+#endif
+  const uint32_t base = min(max(f, 128u) - 128u, 65280u);
+  const uint32_t b2 = base * 0x10001u;
+  const uint4 d0 = make_uint4(q0.x - b2, q0.y - b2, q0.z - b2, q0.w - b2);
+  const uint4 d1 = make_uint4(q1.x - b2, q1.y - b2, q1.z - b2, q1.w - b2);
+  const uint32_t any = d0.x | d0.y | d0.z | d0.w | d1.x | d1.y | d1.z | d1.w;
+#ifdef GPCX_PLANE_SKIP  // timing probe: leave GPCX_PLANE_SKIP of every 4 blocks raw
+  const bool narrow = __all_sync(0xFFFFFFFFu, (any & 0xFF00FF00u) == 0) && (blk & 3) >= GPCX_PLANE_SKIP;
+#else
+  const bool narrow = __all_sync(0xFFFFFFFFu, (any & 0xFF00FF00u) == 0);
+#endif
+#if defined(GPCX_PLANE_PROBE) && GPCX_PLANE_PROBE == 1  // timing probe only (wrong results)
+  if (narrow && lane == 99)
+#else
+  if (narrow)
+#endif
+    st_stream(pres + blk * 32 + lane,
+              make_uint4(__byte_perm(d0.x, d0.y, 0x6420), __byte_perm(d0.z, d0.w, 0x6420),
+                         __byte_perm(d1.x, d1.y, 0x6420), __byte_perm(d1.z, d1.w, 0x6420)));
+  if (lane == 0) pbase[blk] = narrow ? base : kRawBlock;
+}
+
+// count_image over whole blocks (block b = the grid's warp b mod W, the
+// next block's two loads in flight while this one is coded and counted),
+// coding each block into the plane; the < 64 vectors past the last whole
+// block go to the last CTA, uncoded.
+template <int kSwz, bool kFew>
+__device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std::uint64_t n,
+                                                  int cta, int ctas, uint32_t* bins,
+                                                  uint32_t* overflow, uint32_t* pbase,
+                                                  uint4* pres) {
+  const std::uint64_t head = head_len(img, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t nblk = nvec >> 6;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  const uint4* body = reinterpret_cast<const uint4*>(img + head);
+  if (cta == 0)
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one<kSwz>(bins, overflow, img[i]);
+  if (cta == ctas - 1) {
+    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
+      count_one<kSwz>(bins, overflow, img[i]);
+    for (std::uint64_t v = (nblk << 6) + threadIdx.x; v < nvec; v += kThreads)
+      count_vec_plain<kSwz>(bins, overflow, ld_stream(body + v));
+  }
+  const uint32_t lane = threadIdx.x & 31u;
+  const std::uint64_t W = static_cast<std::uint64_t>(ctas) * (kThreads / 32);
+  std::uint64_t b = static_cast<std::uint64_t>(cta) * (kThreads / 32) + (threadIdx.x >> 5);
+  // two register sets used in turn (no copies between stages)
+  uint4 qa0, qa1, qb0, qb1;
+  auto load = [&](std::uint64_t blk, uint4& x0, uint4& x1) {
+    x0 = ld_stream(body + (blk << 6) + lane);
+    x1 = ld_stream(body + (blk << 6) + 32 + lane);
+  };
+  auto work = [&](std::uint64_t blk, uint4 x0, uint4 x1) {
+    code_block(x0, x1, blk, lane, pbase, pres);
+    if constexpr (kFew) {
+      count_pair<kSwz>(bins, overflow, x0, x1);
+    } else {
+      count_vec_plain<kSwz>(bins, overflow, x0);
+      count_vec_plain<kSwz>(bins, overflow, x1);
+    }
+  };
+  if (b < nblk) load(b, qa0, qa1);  // warp-uniform conditions throughout
+  while (b < nblk) {
+    if (b + W < nblk) load(b + W, qb0, qb1);
+    work(b, qa0, qa1);
+    b += W;
+    if (b >= nblk) break;
+    if (b + W < nblk) load(b + W, qa0, qa1);
+    work(b, qb0, qb1);
+    b += W;
+  }
+}
+
+// Block vectors as loaded for the apply: a narrow block's residuals (r0,
+// one 16-byte load), else the two image vectors (r0, r1) -- predicated
+// loads, no branch around them.
+__device__ __forceinline__ void load_block(const uint4* body, const uint4* pres, std::uint64_t b,
+                                           uint32_t lane, uint32_t bw, uint4& r0, uint4& r1) {
+  const uint4* pr = pres + b * 32 + lane;
+  const uint4* p0 = body + (b << 6) + lane;
+  const uint4* p1 = p0 + 32;
+  asm volatile(
+      "{\n .reg .pred c;\n setp.ne.u32 c, %8, %9;\n"
+      " @c ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%10];\n"
+      " @!c ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%11];\n"
+      " @!c ld.global.L1::no_allocate.v4.u32 {%4,%5,%6,%7}, [%12];\n}"
+      : "=r"(r0.x), "=r"(r0.y), "=r"(r0.z), "=r"(r0.w), "=r"(r1.x), "=r"(r1.y), "=r"(r1.z),
+        "=r"(r1.w)
+      : "r"(bw), "r"(kRawBlock), "l"(pr), "l"(p0), "l"(p1));
+}
+__device__ __forceinline__ uint4 expand(uint32_t lo, uint32_t hi, uint32_t b2) {
+  // base + residual <= 65535 per half: no carry between the halves
+  return make_uint4(__byte_perm(lo, 0u, 0x4140) + b2, __byte_perm(lo, 0u, 0x4342) + b2,
+                    __byte_perm(hi, 0u, 0x4140) + b2, __byte_perm(hi, 0u, 0x4342) + b2);
+}
+template <int kSwz>
+__device__ __forceinline__ void store_block(const std::uint16_t* s_lut, uint4* dst, std::uint64_t b,
+                                            uint32_t lane, uint32_t bw, uint4 r0, uint4 r1) {
+  uint4 v0 = r0, v1 = r1;
+  if (bw != kRawBlock) {
+    const uint32_t b2 = bw * 0x10001u;
+    v0 = expand(r0.x, r0.y, b2);
+    v1 = expand(r0.z, r0.w, b2);
+  }
+  st_stream(dst + (b << 6) + lane, lookup_vec<kSwz>(s_lut, v0));
+  st_stream(dst + (b << 6) + 32 + lane, lookup_vec<kSwz>(s_lut, v1));
+}
+
+// apply_image over the count pass's blocks: a block's base word is loaded
+// one stage before the vectors it selects (so the block's loads issue as
+// residuals or image vectors with no dependent wait), the next block's
+// loads in flight while this one is stored; the dynamic tail hands out
+// chunks of 128 blocks (4 per warp).
+template <int kSwz>
+__device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
+                                                  const std::uint16_t* in, std::uint16_t* out,
+                                                  std::uint64_t n, int cta, int ctas,
+                                                  std::uint32_t* tail, const uint32_t* pbase,
+                                                  const uint4* pres) {
+  constexpr std::uint64_t kWarps = kThreads / 32;
+  constexpr std::uint64_t kChunkBlk = 4 * kWarps;  // blocks per tail chunk (128 KiB of image)
+  const std::uint64_t tid = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
+  const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
+  const std::uint64_t head = head_len(in, n);
+  const std::uint64_t nvec = (n - head) >> 3;
+  const std::uint64_t nblk = nvec >> 6;
+  const std::uint64_t tail0 = head + (nvec << 3);
+  if (tid < head) out[tid] = lut_at<kSwz>(s_lut, in[tid]);
+  if (tid < n - tail0) out[tail0 + tid] = lut_at<kSwz>(s_lut, in[tail0 + tid]);
+  const uint4* src = reinterpret_cast<const uint4*>(in + head);
+  uint4* dst = reinterpret_cast<uint4*>(out + head);
+  for (std::uint64_t v = (nblk << 6) + tid; v < nvec; v += stride)
+    st_stream(dst + v, lookup_vec<kSwz>(s_lut, ld_stream(src + v)));
+  const uint32_t lane = threadIdx.x & 31u;
+  const std::uint64_t W = static_cast<std::uint64_t>(ctas) * kWarps;
+  const std::uint64_t tail_chunks = 4ull * static_cast<std::uint64_t>(ctas);
+  const bool dynamic = tail != nullptr && nblk >= 16 * tail_chunks * kChunkBlk;
+  const std::uint64_t static_end = dynamic ? nblk - tail_chunks * kChunkBlk : nblk;
+#ifndef GPCX_PLANE_KU
+#define GPCX_PLANE_KU 2
+#endif
+  constexpr int kU = GPCX_PLANE_KU;  // blocks per stage
+  std::uint64_t b = static_cast<std::uint64_t>(cta) * kWarps + (threadIdx.x >> 5);
+  uint32_t bw[kU] = {}, nbw[kU] = {};
+  uint4 r[kU][2], nr[kU][2];
+  bool have = b + (kU - 1) * W < static_end;  // warp-uniform
+  if (have) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) bw[u] = __ldcg(pbase + b + u * W);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) load_block(src, pres, b + u * W, lane, bw[u], r[u][0], r[u][1]);
+  }
+  if (b + (2 * kU - 1) * W < static_end) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) nbw[u] = __ldcg(pbase + b + (kU + u) * W);
+  }
+  while (have) {
+    const std::uint64_t nx = b + kU * W;
+    const bool nhave = nx + (kU - 1) * W < static_end;
+    if (nhave) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) load_block(src, pres, nx + u * W, lane, nbw[u], nr[u][0], nr[u][1]);
+    }
+    uint32_t nnbw[kU] = {};
+    if (nx + (2 * kU - 1) * W < static_end) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) nnbw[u] = __ldcg(pbase + nx + (kU + u) * W);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) store_block<kSwz>(s_lut, dst, b + u * W, lane, bw[u], r[u][0], r[u][1]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      r[u][0] = nr[u][0];
+      r[u][1] = nr[u][1];
+      bw[u] = nbw[u];
+      nbw[u] = nnbw[u];
+    }
+    b = nx;
+    have = nhave;
+  }
+  for (; b < static_end; b += W) {
+    const uint32_t w = __ldcg(pbase + b);
+    uint4 y0, y1;
+    load_block(src, pres, b, lane, w, y0, y1);
+    store_block<kSwz>(s_lut, dst, b, lane, w, y0, y1);
+  }
+  if (!dynamic) return;
+  __shared__ std::uint32_t s_chunk;
+  for (;;) {
+    __syncthreads();  // the previous chunk index is consumed
+    if (threadIdx.x == 0) s_chunk = atomicAdd(tail, 1u);
+    __syncthreads();
+    const std::uint64_t c = s_chunk;
+    if (c >= tail_chunks) break;
+    const std::uint64_t b0 = static_end + c * kChunkBlk + (threadIdx.x >> 5);
+    uint32_t w[4];
+    uint4 y[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = __ldcg(pbase + b0 + u * kWarps);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load_block(src, pres, b0 + u * kWarps, lane, w[u], y[u][0], y[u][1]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) store_block<kSwz>(s_lut, dst, b0 + u * kWarps, lane, w[u], y[u][0], y[u][1]);
   }
 }
 
@@ -619,9 +877,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                  uint32_t* __restrict__ hist, SliceSummary* __restrict__ blocks, int mode,
                  std::uint16_t* __restrict__ lut, gpcx_lut_stats* __restrict__ stats,
                  int stages, const PeerTable* __restrict__ peers, std::uint32_t seq,
-                 unsigned long long timeout_ns, std::uint32_t* __restrict__ tail) {
+                 unsigned long long timeout_ns, std::uint32_t* __restrict__ tail,
+                 unsigned char* __restrict__ plane) {
   extern __shared__ uint4 smem_u4[];
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem_u4);
+  // residual plane (kCount and kApply in this launch, room in the workspace)
+  uint32_t* pbase = reinterpret_cast<uint32_t*>(plane);
+  uint4* pres = reinterpret_cast<uint4*>(plane + plane_base_bytes(n));
   __shared__ unsigned long long s_wsum[8], s_wfcount[8];
   __shared__ uint32_t s_wfirst[8], s_wlast[8];
   cg::grid_group grid = cg::this_grid();
@@ -637,13 +899,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (count && static_cast<int>(blockIdx.x) < nparts) {
     for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    switch (s_swz & 7u) {
-      case 0: count_image<0, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 1: count_image<1, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 2: count_image<2, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 4: count_image<0, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      case 5: count_image<1, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      default: count_image<2, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+    if (plane != nullptr && (s_swz & 8u) != 0) {
+      switch (s_swz & 7u) {
+        case 0: count_image_coded<0, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+        case 1: count_image_coded<1, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+        case 2: count_image_coded<2, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+        case 4: count_image_coded<0, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+        case 5: count_image_coded<1, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+        default: count_image_coded<2, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
+      }
+    } else {
+      switch (s_swz & 7u) {
+        case 0: count_image<0, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+        case 1: count_image<1, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+        case 2: count_image<2, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
+        case 4: count_image<0, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+        case 5: count_image<1, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+        default: count_image<2, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
+      }
     }
     __syncthreads();
     LUT_STAMP(1);
@@ -846,9 +1119,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   else stage_lut<0>(smem_u4, lut);
   __syncthreads();
   LUT_STAMP(8);
-  if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
-  else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
-  else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  if (plane != nullptr && (s_swz & 8u) != 0) {  // the plane this launch's count pass coded
+    if (layout == 1) apply_image_coded<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
+    else if (layout == 2) apply_image_coded<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
+    else apply_image_coded<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
+  } else {
+    if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+    else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+    else apply_image<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
+  }
 #ifdef GPCX_LUT_TRACE
   __syncthreads();
 #endif
@@ -1107,6 +1386,12 @@ std::uint64_t workspace_bytes() {
   return kPartsOff + static_cast<std::uint64_t>(kMaxParts) * kWords * 4;
 }
 
+std::uint64_t plane_bytes(std::uint64_t n) {
+  return n >= kPlaneMin ? plane_base_bytes(n) + (n >> 9) * 512 : 0;
+}
+
+std::uint64_t workspace_bytes(std::uint64_t n) { return workspace_bytes() + plane_bytes(n); }
+
 int parts_for(std::uint64_t n, int num_sms) {
   // One CTA per SM once there is enough work; at least 64 Ki samples per
   // CTA below that so the per-CTA partial flush stays amortised.
@@ -1117,12 +1402,26 @@ int parts_for(std::uint64_t n, int num_sms) {
 
 namespace {
 // fused_kernel over the whole device (see its comment for `stages`).
+// GPCX_LUT_PLANE=0: never code the residual plane (A/B only).
+bool plane_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("GPCX_LUT_PLANE");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
+}
+
 void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std::uint64_t n,
                   uint32_t* hist, int mode, std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
                   cudaStream_t stream, const PeerTable* peers = nullptr, std::uint32_t seq = 0,
-                  unsigned long long timeout_ns = 0) {
+                  unsigned long long timeout_ns = 0, std::uint64_t ws_bytes = 0) {
   set_attrs_once();
   auto* base = static_cast<unsigned char*>(ws);
+  // the residual plane: count and apply in this launch, a plane-sized workspace
+  unsigned char* plane = nullptr;
+  if ((stages & (kCount | kApply)) == (kCount | kApply) && plane_bytes(n) != 0 &&
+      ws_bytes >= workspace_bytes(n) && plane_enabled())
+    plane = base + workspace_bytes();
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
   auto* parts = reinterpret_cast<uint32_t*>(base + kPartsOff);
   auto* blocks = reinterpret_cast<SliceSummary*>(base + kBlocksOff);
@@ -1132,7 +1431,7 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
   int nparts = parts_for(n, sms);
   void* args[] = {const_cast<std::uint16_t**>(&img), &out, &n, &nparts, &parts, &overflow,
                   &hist, &blocks, &mode, &lut, &stats, &stages,
-                  const_cast<PeerTable**>(&peers), &seq, &timeout_ns, &tail};
+                  const_cast<PeerTable**>(&peers), &seq, &timeout_ns, &tail, &plane};
   GPCX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fused_kernel),
                                         dim3(std::max(sms, kSlices)), dim3(kThreads), args,
                                         kSmemHist, stream));
@@ -1181,9 +1480,11 @@ void launch_hist_lut(const std::uint16_t* img, std::uint64_t n, int mode, std::u
 }
 
 void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n, int mode,
-                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream) {
+                    std::uint16_t* lut, gpcx_lut_stats* stats, void* ws, cudaStream_t stream,
+                    std::uint64_t ws_bytes) {
   if (mode == GPCX_LUT_EQUALIZE && co_aligned(in, out) && n != 0) {
-    launch_fused(kCount | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream);
+    launch_fused(kCount | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream,
+                 nullptr, 0, 0, ws_bytes);
     return;
   }
   if (mode == GPCX_LUT_STRETCH && co_aligned(in, out) && n != 0 && stretch_fused_enabled()) {
@@ -1208,13 +1509,13 @@ void launch_correct(const std::uint16_t* in, std::uint16_t* out, std::uint64_t n
 void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::uint32_t seq,
                          std::uint64_t timeout_ns, const std::uint16_t* in, std::uint16_t* out,
                          std::uint64_t n, int mode, std::uint16_t* lut, gpcx_lut_stats* stats,
-                         void* ws, cudaStream_t stream) {
+                         void* ws, cudaStream_t stream, std::uint64_t ws_bytes) {
   // every rank launches the same stages (the rendezvous sits in phase 2);
   // the apply needs co-aligned in/out (the callers check) or out == nullptr
   const bool fused_apply = out != nullptr && co_aligned(in, out);
   const int stages = kCount | kExchange | kBuild | (fused_apply ? kApply : 0);
   launch_fused(stages, in, fused_apply ? out : nullptr, n, own_hist, mode, lut, stats, ws,
-               stream, table, seq, timeout_ns);
+               stream, table, seq, timeout_ns, ws_bytes);
   if (out != nullptr && !fused_apply) launch_apply(lut, in, out, n, stream);
 }
 

@@ -2,7 +2,7 @@
 // stamps of thread 0 of every CTA; design exploration, not product code).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DGPCX_LUT_TRACE \
 //        -o tools/fused_trace tools/fused_trace.cu paper_1505_05655_b200/csrc/status.cpp
-//   ./tools/fused_trace [rows cols]
+//   ./tools/fused_trace [rows cols [r|u]]   (GPCX_LUT_PLANE=0: no residual plane)
 #include "../paper_1505_05655_b200/csrc/lut.cu"
 
 // the library's device-health hook (host/runtime.cpp) is not linked here
@@ -17,12 +17,15 @@ void note_cuda_error(cudaError_t, const char*) {}
 int main(int argc, char** argv) {
   const std::uint64_t rows = argc > 2 ? std::strtoull(argv[1], nullptr, 10) : 4096;
   const std::uint64_t cols = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 4096;
+  const bool noise = argc > 3 && argv[3][0] == 'u';  // "u": uniform16-like noise
   const std::uint64_t n = rows * cols;
   std::vector<std::uint16_t> h(n);
   for (std::uint64_t r = 0; r < rows; ++r)
     for (std::uint64_t c = 0; c < cols; ++c)
-      h[r * cols + c] = static_cast<std::uint16_t>(1024 + 3071 * (r + c) / (rows + cols - 2) +
-                                                   ((r * 7919 + c * 104729) & 63) - 32);
+      h[r * cols + c] =
+          noise ? static_cast<std::uint16_t>(((r * cols + c) * 0x9E3779B97F4A7C15ull) >> 48)
+                : static_cast<std::uint16_t>(1024 + 3071 * (r + c) / (rows + cols - 2) +
+                                             ((r * 7919 + c * 104729) & 63) - 32);
   std::uint16_t *img, *out, *lut;
   void* ws;
   gpcx_lut_stats* stats;
@@ -31,8 +34,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&out, n * 2);
   cudaMalloc(&lut, 131072);
   cudaMalloc(&stats, sizeof(gpcx_lut_stats));
-  cudaMalloc(&ws, gpcx::lut::workspace_bytes());
-  cudaMemset(ws, 0, gpcx::lut::workspace_bytes());
+  const std::uint64_t ws_bytes = gpcx::lut::workspace_bytes(n);  // room for the residual plane
+  cudaMalloc(&ws, ws_bytes);
+  cudaMemset(ws, 0, ws_bytes);
   const int sms = gpcx::device_sm_count();
   cudaMalloc(&trace, sms * 16 * 8);
   cudaMemcpyToSymbol(gpcx::lut::g_lut_trace, &trace, sizeof(trace));
@@ -49,7 +53,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    gpcx::lut::launch_correct(img, out, n, GPCX_LUT_EQUALIZE, lut, stats, ws, nullptr);
+    gpcx::lut::launch_correct(img, out, n, GPCX_LUT_EQUALIZE, lut, stats, ws, nullptr, ws_bytes);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
