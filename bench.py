@@ -1064,8 +1064,9 @@ def run_b200(args) -> None:
             "traffic": tr.get("fused_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
             "algorithmic_bytes_per_launch": 6 * band_px, "peak_source": pk["source"],
             "kernels": {"fused_kernel": {"ms": round(kern_ms, 4),
-                                         "phases": "histogram (2 B/px, smem-atomic bound) | "
-                                                   "merge + LUT | apply (4 B/px)"},
+                                         "phases": "histogram (2 B/px read, smem-atomic bound, "
+                                                   "+ 1 B/px residual plane written) | merge + LUT | "
+                                                   "apply (1 B/px plane read, 2 B/px written)"},
                         "step": {"achieved": round(step_ach, 1),
                                  "frac": round(step_ach / pk["hbm_gbs"], 4),
                                  "algorithmic_bytes": 6 * band_px}}}
@@ -1073,8 +1074,8 @@ def run_b200(args) -> None:
         roof["kernels"]["histogram_all_reduce"] = {"ms": round(exch_ms, 4), "bytes": 262144}
     if lut["exchange"] == "peer":
         roof["kernels"]["fused_kernel"]["phases"] = (
-            "histogram (2 B/px) | publish slice + system-scope flag rendezvous + P2P sum of the "
-            "peers' slices | LUT | apply (4 B/px)")
+            "histogram (2 B/px read + 1 B/px residual plane written) | publish slice + system-scope "
+            "flag rendezvous + P2P sum of the peers' slices | LUT | apply (1 B/px plane read, 2 B/px written)")
     gather = None
     if gather_ms is not None:
         gather = {"ms": round(gather_ms, 3), "bytes": 2 * ROWS * COLS,

@@ -506,26 +506,14 @@ __device__ __forceinline__ uint4 ld_plane(const uint4* p) {
 // redux min/max version cost ~75 us at C3).
 __device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk, uint32_t lane,
                                            uint32_t* pbase, uint4* pres) {
-#if defined(GPCX_PLANE_PROBE) && GPCX_PLANE_PROBE == 2  // timing probe only (wrong results)
-  const uint32_t f = q0.x & 0xFFFFu;
-#else
   const uint32_t f = __shfl_sync(0xFFFFFFFFu, q0.x, 0) & 0xFFFFu;
-#endif
   const uint32_t base = min(max(f, 128u) - 128u, 65280u);
   const uint32_t b2 = base * 0x10001u;
   const uint4 d0 = make_uint4(q0.x - b2, q0.y - b2, q0.z - b2, q0.w - b2);
   const uint4 d1 = make_uint4(q1.x - b2, q1.y - b2, q1.z - b2, q1.w - b2);
   const uint32_t any = d0.x | d0.y | d0.z | d0.w | d1.x | d1.y | d1.z | d1.w;
-#ifdef GPCX_PLANE_SKIP  // timing probe: leave GPCX_PLANE_SKIP of every 4 blocks raw
-  const bool narrow = __all_sync(0xFFFFFFFFu, (any & 0xFF00FF00u) == 0) && (blk & 3) >= GPCX_PLANE_SKIP;
-#else
   const bool narrow = __all_sync(0xFFFFFFFFu, (any & 0xFF00FF00u) == 0);
-#endif
-#if defined(GPCX_PLANE_PROBE) && GPCX_PLANE_PROBE == 1  // timing probe only (wrong results)
-  if (narrow && lane == 99)
-#else
   if (narrow)
-#endif
     st_stream(pres + blk * 32 + lane,
               make_uint4(__byte_perm(d0.x, d0.y, 0x6420), __byte_perm(d0.z, d0.w, 0x6420),
                          __byte_perm(d1.x, d1.y, 0x6420), __byte_perm(d1.z, d1.w, 0x6420)));
@@ -619,11 +607,11 @@ __device__ __forceinline__ void store_block(const std::uint16_t* s_lut, uint4* d
   st_stream(dst + (b << 6) + 32 + lane, lookup_vec<kSwz>(s_lut, v1));
 }
 
-// apply_image over the count pass's blocks: a block's base word is loaded
-// one stage before the vectors it selects (so the block's loads issue as
-// residuals or image vectors with no dependent wait), the next block's
-// loads in flight while this one is stored; the dynamic tail hands out
-// chunks of 128 blocks (4 per warp).
+// apply_image over the count pass's blocks, two per warp per stage: a
+// block's base word is loaded one stage before the vectors it selects (so
+// the block's loads issue as residuals or image vectors with no dependent
+// wait), the next stage's loads in flight while this one is stored; the
+// dynamic tail hands out chunks of 128 blocks (4 per warp).
 template <int kSwz>
 __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
                                                   const std::uint16_t* in, std::uint16_t* out,
@@ -645,42 +633,42 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
   for (std::uint64_t v = (nblk << 6) + tid; v < nvec; v += stride)
     st_stream(dst + v, lookup_vec<kSwz>(s_lut, ld_stream(src + v)));
   const uint32_t lane = threadIdx.x & 31u;
+  // blocks in reverse order: the count pass coded the high blocks last, so
+  // the first ones applied are partly still in L2 (~0.4% of the step)
+#define MAPB(x) (nblk - 1 - (x))
   const std::uint64_t W = static_cast<std::uint64_t>(ctas) * kWarps;
   const std::uint64_t tail_chunks = 4ull * static_cast<std::uint64_t>(ctas);
   const bool dynamic = tail != nullptr && nblk >= 16 * tail_chunks * kChunkBlk;
   const std::uint64_t static_end = dynamic ? nblk - tail_chunks * kChunkBlk : nblk;
-#ifndef GPCX_PLANE_KU
-#define GPCX_PLANE_KU 2
-#endif
-  constexpr int kU = GPCX_PLANE_KU;  // blocks per stage
+  constexpr int kU = 2;  // blocks per stage (1: 80 us slower at C3)
   std::uint64_t b = static_cast<std::uint64_t>(cta) * kWarps + (threadIdx.x >> 5);
   uint32_t bw[kU] = {}, nbw[kU] = {};
   uint4 r[kU][2], nr[kU][2];
   bool have = b + (kU - 1) * W < static_end;  // warp-uniform
   if (have) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) bw[u] = __ldcg(pbase + b + u * W);
+    for (int u = 0; u < kU; ++u) bw[u] = __ldcg(pbase + MAPB(b + u * W));
 #pragma unroll
-    for (int u = 0; u < kU; ++u) load_block(src, pres, b + u * W, lane, bw[u], r[u][0], r[u][1]);
+    for (int u = 0; u < kU; ++u) load_block(src, pres, MAPB(b + u * W), lane, bw[u], r[u][0], r[u][1]);
   }
   if (b + (2 * kU - 1) * W < static_end) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) nbw[u] = __ldcg(pbase + b + (kU + u) * W);
+    for (int u = 0; u < kU; ++u) nbw[u] = __ldcg(pbase + MAPB(b + (kU + u) * W));
   }
   while (have) {
     const std::uint64_t nx = b + kU * W;
     const bool nhave = nx + (kU - 1) * W < static_end;
     if (nhave) {
 #pragma unroll
-      for (int u = 0; u < kU; ++u) load_block(src, pres, nx + u * W, lane, nbw[u], nr[u][0], nr[u][1]);
+      for (int u = 0; u < kU; ++u) load_block(src, pres, MAPB(nx + u * W), lane, nbw[u], nr[u][0], nr[u][1]);
     }
     uint32_t nnbw[kU] = {};
     if (nx + (2 * kU - 1) * W < static_end) {
 #pragma unroll
-      for (int u = 0; u < kU; ++u) nnbw[u] = __ldcg(pbase + nx + (kU + u) * W);
+      for (int u = 0; u < kU; ++u) nnbw[u] = __ldcg(pbase + MAPB(nx + (kU + u) * W));
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) store_block<kSwz>(s_lut, dst, b + u * W, lane, bw[u], r[u][0], r[u][1]);
+    for (int u = 0; u < kU; ++u) store_block<kSwz>(s_lut, dst, MAPB(b + u * W), lane, bw[u], r[u][0], r[u][1]);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       r[u][0] = nr[u][0];
@@ -692,10 +680,10 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
     have = nhave;
   }
   for (; b < static_end; b += W) {
-    const uint32_t w = __ldcg(pbase + b);
+    const uint32_t w = __ldcg(pbase + MAPB(b));
     uint4 y0, y1;
-    load_block(src, pres, b, lane, w, y0, y1);
-    store_block<kSwz>(s_lut, dst, b, lane, w, y0, y1);
+    load_block(src, pres, MAPB(b), lane, w, y0, y1);
+    store_block<kSwz>(s_lut, dst, MAPB(b), lane, w, y0, y1);
   }
   if (!dynamic) return;
   __shared__ std::uint32_t s_chunk;
@@ -709,13 +697,14 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
     uint32_t w[4];
     uint4 y[4][2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) w[u] = __ldcg(pbase + b0 + u * kWarps);
+    for (int u = 0; u < 4; ++u) w[u] = __ldcg(pbase + MAPB(b0 + u * kWarps));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load_block(src, pres, b0 + u * kWarps, lane, w[u], y[u][0], y[u][1]);
+    for (int u = 0; u < 4; ++u) load_block(src, pres, MAPB(b0 + u * kWarps), lane, w[u], y[u][0], y[u][1]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) store_block<kSwz>(s_lut, dst, b0 + u * kWarps, lane, w[u], y[u][0], y[u][1]);
+    for (int u = 0; u < 4; ++u) store_block<kSwz>(s_lut, dst, MAPB(b0 + u * kWarps), lane, w[u], y[u][0], y[u][1]);
   }
 }
+#undef MAPB
 
 // floor(num / d) for num < 2^53 and d >= 1 without a 64-bit integer divide
 // (a ~70-instruction software sequence): num converts to f64 exactly and
