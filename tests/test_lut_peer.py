@@ -99,6 +99,7 @@ def _run_group(tmp_path, nranks, rows, cols, kind, seed, steps, modes):
     (2, 4096, 4096, 1),    # uniform16: every bin populated
     (3, 2049, 1024, 0),    # three ranks, uneven split
     (3, 2, 5, 1),          # rank 2's band is empty: it still meets its peers
+    (2, 8192, 8200, 0),    # bands >= 2^25 samples: the residual plane in the peer launch
 ])
 def test_peer_exchange_equals_single_device_oracle(shared_gpu, tmp_path, nranks, rows, cols, kind):
     from oracle import oracle as O
