@@ -185,8 +185,14 @@ void gpcx_pinned_free(void* ptr);
 /* Used by the executor / planner and by bench.py's device-timed leg.   */
 /* ------------------------------------------------------------------ */
 
-/* Workspace (device bytes) a LUT call over n pixels needs.  Workspace must
- * be zero-filled ONCE when allocated; the kernels leave it zeroed again. */
+/* Workspace (device bytes) recommended for a LUT call over n pixels.
+ * Workspace must be zero-filled ONCE when allocated; the kernels leave it
+ * zeroed again.  From 2^25 pixels the size includes the residual plane
+ * (~1 byte per pixel) through which the equalize LUT_CORRECT entry points
+ * (gpcx_lut_correct_device, gpcx_lut_correct_peer_device) move the image
+ * from their count pass to their apply pass at 1 instead of 2 B/px; a
+ * workspace of at least gpcx_lut_workspace_size(1, .) bytes (the fixed
+ * part) is accepted by every call and only gives up that plane. */
 int gpcx_lut_workspace_size(uint64_t n, uint64_t* bytes);
 /* 65536-bin u32 histogram of n u16 samples (n < 2^32). */
 int gpcx_lut_hist_device(const uint16_t* img, uint64_t n, uint32_t* hist,
