@@ -182,6 +182,43 @@ __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
   }
 }
 
+// Two vectors (16 samples) per lane: the 16 returning atomics back to back,
+// then ONE conservative wrap test for all of them -- does any half of any
+// returned word read 0xFFFF? (a SIMD u16x2 max over the 16 old values) --
+// and the exact per-sample check only when it fires.  The count pass is
+// instruction-issue bound, not atomic-unit bound: the exact per-sample
+// test (mask select, and, compare: 3 instructions per sample) and its
+// branch cost ~30% of the pass (C3 uniform16 count 0.49 -> 0.35 ms without
+// them, profiles/r2/plane_trace.txt).  The test can fire spuriously (the
+// other bin of a word at 0xFFFF); the slow path then finds nothing.
+template <int kSwz>
+__device__ __forceinline__ void count_pair_plain(uint32_t* bins, uint32_t* overflow, uint4 q0,
+                                                 uint4 q1) {
+  const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+  uint32_t old[16];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;
+    old[2 * j] = atomicAdd(&bins[word_of<kSwz>(lo)], (lo & 1u) ? 0x10000u : 1u);
+    old[2 * j + 1] = atomicAdd(&bins[word_of<kSwz>(hi)], (hi & 1u) ? 0x10000u : 1u);
+  }
+  uint32_t mx = __vmaxu2(__vmaxu2(old[0], old[1]), __vmaxu2(old[2], old[3]));
+  mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(old[4], old[5]), __vmaxu2(old[6], old[7])));
+  mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(old[8], old[9]), __vmaxu2(old[10], old[11])));
+  mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(old[12], old[13]), __vmaxu2(old[14], old[15])));
+  if ((mx & 0xFFFFu) != 0xFFFFu && mx < 0xFFFF0000u) return;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t v = (j & 1) ? w[j >> 1] >> 16 : w[j >> 1] & 0xFFFFu;
+    const uint32_t hi_bin = v & 1u;
+    const uint32_t m = hi_bin ? 0xFFFF0000u : 0x0000FFFFu;
+    if ((old[j] & m) != m) continue;
+    atomicAdd(&overflow[v], 65536u);
+    if (!hi_bin)
+      atomicAdd(&overflow[v + 1], (old[j] >> 16) == 0xFFFFu ? 65535u : 0xFFFFFFFFu);
+  }
+}
+
 // Repetitive data (flat regions, binary or few-level images): on one word
 // the lanes' returning atomics queue up, so a warp whose samples fall on
 // few banks combines them first -- one or two atomics when the warp vector
@@ -258,8 +295,7 @@ __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, u
     count_vec_few<kSwz>(bins, overflow, q0, mask);
     count_vec_few<kSwz>(bins, overflow, q1, mask);
   } else {
-    count_vec_plain<kSwz>(bins, overflow, q0);
-    count_vec_plain<kSwz>(bins, overflow, q1);
+    count_pair_plain<kSwz>(bins, overflow, q0, q1);
   }
 }
 
@@ -384,8 +420,7 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
     if constexpr (kFew) {
       count_pair<kSwz>(bins, overflow, q[0], q[1]);
     } else {
-      count_vec_plain<kSwz>(bins, overflow, q[0]);
-      count_vec_plain<kSwz>(bins, overflow, q[1]);
+      count_pair_plain<kSwz>(bins, overflow, q[0], q[1]);
     }
     q[0] = nq[0];
     q[1] = nq[1];
@@ -556,8 +591,7 @@ __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std:
     if constexpr (kFew) {
       count_pair<kSwz>(bins, overflow, x0, x1);
     } else {
-      count_vec_plain<kSwz>(bins, overflow, x0);
-      count_vec_plain<kSwz>(bins, overflow, x1);
+      count_pair_plain<kSwz>(bins, overflow, x0, x1);
     }
   };
   if (b < nblk) load(b, qa0, qa1);  // warp-uniform conditions throughout
