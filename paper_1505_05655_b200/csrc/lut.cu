@@ -185,11 +185,12 @@ __device__ __forceinline__ void count_vec_plain(uint32_t* bins,
 // Two vectors (16 samples) per lane: the 16 returning atomics back to back,
 // then ONE conservative wrap test for all of them -- does any half of any
 // returned word read 0xFFFF? (a SIMD u16x2 max over the 16 old values) --
-// and the exact per-sample check only when it fires.  The count pass is
-// instruction-issue bound, not atomic-unit bound: the exact per-sample
+// and the exact per-sample check only when it fires.  The exact per-sample
 // test (mask select, and, compare: 3 instructions per sample) and its
-// branch cost ~30% of the pass (C3 uniform16 count 0.49 -> 0.35 ms without
-// them, profiles/r2/plane_trace.txt).  The test can fire spuriously (the
+// branch cost ~3% of the pass on the C3 scenes, whose random noise makes
+// the atomics bank-conflict bound (count 493 -> 478 us), and ~30% where
+// the samples of a warp fall on distinct banks and the pass becomes issue
+// bound (profiles/r2/plane_trace.txt).  The test can fire spuriously (the
 // other bin of a word at 0xFFFF); the slow path then finds nothing.
 template <int kSwz>
 __device__ __forceinline__ void count_pair_plain(uint32_t* bins, uint32_t* overflow, uint4 q0,

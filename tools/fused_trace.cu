@@ -2,8 +2,9 @@
 // stamps of thread 0 of every CTA; design exploration, not product code).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DGPCX_LUT_TRACE \
 //        -o tools/fused_trace tools/fused_trace.cu paper_1505_05655_b200/csrc/status.cpp
-//   ./tools/fused_trace [rows cols [r|u]]   (GPCX_LUT_PLANE=0: no residual plane)
+//   ./tools/fused_trace [rows cols [r|u]]   (bench.py's ramp12 / uniform16 scenes)   (GPCX_LUT_PLANE=0: no residual plane)
 #include "../paper_1505_05655_b200/csrc/lut.cu"
+#include "../paper_1505_05655_b200/csrc/synth.cu"  // the bench's ramp12 / uniform16 scenes
 
 // the library's device-health hook (host/runtime.cpp) is not linked here
 namespace gpcx::rt {
@@ -17,15 +18,8 @@ void note_cuda_error(cudaError_t, const char*) {}
 int main(int argc, char** argv) {
   const std::uint64_t rows = argc > 2 ? std::strtoull(argv[1], nullptr, 10) : 4096;
   const std::uint64_t cols = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 4096;
-  const bool noise = argc > 3 && argv[3][0] == 'u';  // "u": uniform16-like noise
+  const int kind = argc > 3 && argv[3][0] == 'u' ? 1 : 0;  // r: ramp12, u: uniform16 (seed 0x5eed)
   const std::uint64_t n = rows * cols;
-  std::vector<std::uint16_t> h(n);
-  for (std::uint64_t r = 0; r < rows; ++r)
-    for (std::uint64_t c = 0; c < cols; ++c)
-      h[r * cols + c] =
-          noise ? static_cast<std::uint16_t>(((r * cols + c) * 0x9E3779B97F4A7C15ull) >> 48)
-                : static_cast<std::uint16_t>(1024 + 3071 * (r + c) / (rows + cols - 2) +
-                                             ((r * 7919 + c * 104729) & 63) - 32);
   std::uint16_t *img, *out, *lut;
   void* ws;
   gpcx_lut_stats* stats;
@@ -40,7 +34,8 @@ int main(int argc, char** argv) {
   const int sms = gpcx::device_sm_count();
   cudaMalloc(&trace, sms * 16 * 8);
   cudaMemcpyToSymbol(gpcx::lut::g_lut_trace, &trace, sizeof(trace));
-  cudaMemcpy(img, h.data(), n * 2, cudaMemcpyHostToDevice);
+  gpcx::synth::launch_image(kind, 0x5EED, rows, cols, 0, rows, img, nullptr);
+  cudaDeviceSynchronize();
   char* flush;
   cudaMalloc(&flush, 512 << 20);
   const char* names[] = {"start", "counted", "flushed", "sync1", "merged", "sync2",
