@@ -204,6 +204,7 @@ def _load_ref() -> C.CDLL | None:
         "ref_server_stop": ([vp], i32),
         "ref_submit": ([cp, i32, cp, cp, vp, sz, cp, vp, sz, C.POINTER(C.c_size_t), cp, cp, cp], i32),
         "ref_demosaic": ([i32, i32, cp, sz, sz, vp, vp, i32], i32),
+        "ref_normal_system": ([vp, vp, sz, i32, vp, vp], i32),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -279,6 +280,20 @@ def ref_demosaic(gradient: bool, img: np.ndarray, rows: int, cols: int, phase: s
     ref_check(ref.ref_demosaic(int(gradient), int(gpcref), phase.encode(), rows, cols,
                                img.ctypes.data, out.ctypes.data, workers))
     return out
+
+
+def ref_normal_system(xs: np.ndarray, ys: np.ndarray, order: int) -> tuple[np.ndarray, np.ndarray]:
+    """The reference's normal equations (gpc::lsq::build_normal_system,
+    proj/src/lsq.cpp:69-90): A = V^T V ((order+1)^2, f64) and b = V^T y with
+    V[i][j] = xs[i]^j -- contractions computed by the reference itself."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    ys = np.ascontiguousarray(ys, dtype=np.float64)
+    m1 = order + 1
+    a = np.empty((m1, m1), dtype=np.float64)
+    b = np.empty(m1, dtype=np.float64)
+    ref_check(ref.ref_normal_system(xs.ctypes.data, ys.ctypes.data, xs.size, order,
+                                    a.ctypes.data, b.ctypes.data))
+    return a, b
 
 
 def host_cpu() -> dict:

@@ -21,6 +21,7 @@
 #include "gpc/demosaic.hpp"
 #include "gpc/devinfo.hpp"
 #include "gpc/error.hpp"
+#include "gpc/lsq.hpp"
 #include "gpc/registry.hpp"
 #include "gpc/server.hpp"
 #include "gpc/tasks.hpp"
@@ -393,6 +394,21 @@ int ref_demosaic(int gradient, int use_gpcref, const char* phase, std::size_t ro
     std::memcpy(rgb, out.r.data(), n * 2);
     std::memcpy(rgb + n, out.g.data(), n * 2);
     std::memcpy(rgb + 2 * n, out.b.data(), n * 2);
+  });
+}
+
+// The reference's normal equations for a polynomial fit of `order`:
+// A = V^T V ((order+1)^2 Hankel matrix of power sums, row-major) and
+// b = V^T y with V[i][j] = xs[i]^j -- two contractions the reference itself
+// computes (gpc::lsq::build_normal_system, proj/src/lsq.cpp:69-90), used to
+// anchor the MATMUL oracle and the B200 MATMUL on reference-computed values.
+int ref_normal_system(const double* xs, const double* ys, std::size_t n, int order,
+                      double* a_out, double* b_out) {
+  return guarded([&] {
+    const lsq::NormalSystem sys = lsq::build_normal_system(
+        std::span<const double>(xs, n), std::span<const double>(ys, n), order, par::ExecPlan{});
+    std::memcpy(a_out, sys.a.a.data(), sys.a.a.size() * sizeof(double));
+    std::memcpy(b_out, sys.b.data(), sys.b.size() * sizeof(double));
   });
 }
 
