@@ -1,6 +1,7 @@
 // gpcx_serve.cpp -- `gpcx-serve`: the B200 task server as a process, the
 // counterpart of the reference CLI's `gpc serve` (proj/tools/gpc.cpp:94-128):
-// same flags where they apply (--bind, --port, --max-tasks, --timeout), the
+// same flags where they apply (--bind, --port, --max-tasks, --timeout /
+// --timeout-secs), the
 // same shutdown (SIGINT / SIGTERM blocked before the server threads exist,
 // consumed by sigwait, then a draining stop) and a one-line banner.  The
 // registry it serves is libgpcx's: LUT_GEN / LUT_APPLY / LUT_CORRECT /
@@ -65,7 +66,7 @@ int main(int argc, char** argv) {
       port = n;
     } else if (a == "--max-tasks" && parse_int(v, 0, 4096, &n)) {
       max_tasks = n;
-    } else if (a == "--timeout" && parse_int(v, 1, 86400, &n)) {
+    } else if ((a == "--timeout" || a == "--timeout-secs") && parse_int(v, 1, 86400, &n)) {
       timeout_secs = n;
     } else if (a == "--max-pending" && parse_int(v, 1, 1 << 20, &n)) {
       // admission control of the staged server (include/gpcx.h): read from
