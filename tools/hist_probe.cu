@@ -21,6 +21,10 @@
 //      the window to red.global (224 KiB of smem)
 //   15 the same with u8 quads (window of 7168 values), wrap check per byte
 //   16 mode 14 with red (no return, no wrap check): its upper bound
+//   17 u32 WINDOW: values in [900, 900 + 16384) one u32 counter each (64 KiB,
+//      no packing, no wraps) with red.shared; the rest to red.global
+//   18 mode 17 with returning atom (old value folded into a dummy)
+//   19 mode 0 through atomicAdd (compiler-emitted RED, no asm memory clobber)
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -61,13 +65,14 @@ template <int MODE>
 __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh) {
   extern __shared__ uint4 sm[];
   uint32_t* bins = (uint32_t*)sm;
-  constexpr int kZero = MODE == 9 ? 12288 : (MODE >= 14 ? 14336 : 8192);
+  constexpr int kZero = MODE == 9 ? 12288 : ((MODE >= 14 && MODE <= 16) ? 14336 : 8192);
   for (int i = threadIdx.x; i < kZero; i += 1024) sm[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* mine = gh + (uint64_t)blockIdx.x * 65536;
   const uint4* body = (const uint4*)img;
   const uint64_t nvec = n / 8, stride = (uint64_t)gridDim.x * 1024;
+  uint32_t dummy = 0;
   auto px = [&](uint32_t v, int slot) {
     const uint32_t inc = 1u << ((v & 1) << 4);
     if (MODE == 0) reds(bins, v >> 1, inc);
@@ -94,6 +99,15 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
         const uint32_t old = atomicAdd(bins + (d >> 2) * 32u + lane, 1u << sh);
         if (((old >> sh) & 0xFFu) == 0xFFu) redg(mine + v, 256);
       } else redg(mine + v, 1);
+    }
+    else if (MODE == 17) {
+      const uint32_t d = v - 900u;
+      if (d < 16384u) reds(bins, d, 1u); else redg(mine + v, 1);
+    } else if (MODE == 18) {
+      const uint32_t d = v - 900u;
+      if (d < 16384u) dummy ^= atomicAdd(bins + d, 1u); else redg(mine + v, 1);
+    } else if (MODE == 19) {
+      atomicAdd(bins + (v >> 1), inc);
     }
     else if (MODE == 12) { if ((slot & 15) == 15) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 13) { if ((slot & 31) == 31) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
@@ -129,6 +143,7 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
     for (int u = 0; u < 4; ++u) vec(q[u]);
   }
   for (; i < nvec; i += stride) vec(ldnc(body + i));
+  if (dummy == 0x12345u) gh[0] = dummy;
   __syncthreads();
   uint4* dst = (uint4*)(parts + (uint64_t)blockIdx.x * 32768);
   for (int j = threadIdx.x; j < 8192; j += 1024) dst[j] = sm[j];
@@ -136,7 +151,7 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
 
 template <int MODE>
 void run(const char* name, const uint16_t* img, uint64_t n, uint32_t* parts, uint32_t* gh, int sms) {
-  const int smem = MODE == 9 ? 3 * 65536 : (MODE >= 14 ? 14336 * 16 : 131072);
+  const int smem = MODE == 9 ? 3 * 65536 : ((MODE >= 14 && MODE <= 16) ? 14336 * 16 : 131072);
   cudaFuncSetAttribute(hist<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -187,6 +202,9 @@ int main() {
     run<14>("14 lane-private u16 window", img, n, parts, gh, sms);
     run<15>("15 lane-private u8 window", img, n, parts, gh, sms);
     run<16>("16 lane-private u16, red only", img, n, parts, gh, sms);
+    run<17>("17 u32 window red", img, n, parts, gh, sms);
+    run<18>("18 u32 window atom (return)", img, n, parts, gh, sms);
+    run<19>("19 packed u16 via atomicAdd", img, n, parts, gh, sms);
   }
   return 0;
 }
