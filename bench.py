@@ -1064,8 +1064,8 @@ def run_b200(args) -> None:
             "traffic": tr.get("fused_kernel", {}).get("bytes_per_launch_at", {}).get(str(band_px)),
             "algorithmic_bytes_per_launch": 6 * band_px, "peak_source": pk["source"],
             "kernels": {"fused_kernel": {"ms": round(kern_ms, 4),
-                                         "phases": "histogram (2 B/px read, smem-atomic bound, "
-                                                   "+ 1 B/px residual plane written) | merge + LUT | "
+                                         "phases": "histogram (2 B/px read into a u32 smem window / packed "
+                                                   "u16 bins, + 1 B/px residual plane written) | merge + LUT | "
                                                    "apply (1 B/px plane read, 2 B/px written)"},
                         "step": {"achieved": round(step_ach, 1),
                                  "frac": round(step_ach / pk["hbm_gbs"], 4),

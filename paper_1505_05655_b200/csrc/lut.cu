@@ -56,7 +56,7 @@ constexpr std::uint64_t kHistOff = 256 * 1024;
 constexpr std::uint64_t kMinMaxOff = 512 * 1024;
 constexpr std::uint64_t kBlocksOff = kMinMaxOff + 4 * 1024;  // 128 slice summaries (2 KiB)
 constexpr std::uint64_t kPartsOff = kMinMaxOff + 8 * 1024;
-constexpr int kSmemHist = kWords * 4;  // 128 KiB
+constexpr int kSmemHist = kWords * 4 + 65536;  // 128 KiB packed bins + the 64 KiB u32 window
 constexpr int kSmemLut = kBins * 2;    // 128 KiB
 constexpr int kUnroll = 4;
 
@@ -300,6 +300,89 @@ __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, u
   }
 }
 
+// ---- count policies: how one sample / vector / two vectors are counted --
+constexpr uint32_t kWinBins = 16384;   // u32 window counters, 64 KiB of smem
+constexpr uint32_t kNoWindow = 0xFFFFFFFFu;
+
+template <int kSwz>
+struct PlainCounter {  // packed u16 pairs, returning atomics, wrap test
+  uint32_t* bins;
+  uint32_t* overflow;
+  __device__ __forceinline__ void one(uint32_t v) const { count_one<kSwz>(bins, overflow, v); }
+  __device__ __forceinline__ void vec(uint4 q) const { count_vec_plain<kSwz>(bins, overflow, q); }
+  __device__ __forceinline__ void pair(uint4 a, uint4 b) const {
+    count_pair_plain<kSwz>(bins, overflow, a, b);
+  }
+};
+template <int kSwz>
+struct FewCounter {  // repetitive data: warp-combined counts (count_vec_few)
+  uint32_t* bins;
+  uint32_t* overflow;
+  __device__ __forceinline__ void one(uint32_t v) const { count_one<kSwz>(bins, overflow, v); }
+  __device__ __forceinline__ void vec(uint4 q) const { count_vec<kSwz>(bins, overflow, q); }
+  __device__ __forceinline__ void pair(uint4 a, uint4 b) const {
+    count_pair<kSwz>(bins, overflow, a, b);
+  }
+};
+// Narrow data (the sampled values span < kWinBins - 2048): every value in
+// [lo, lo + kWinBins) has its own u32 counter in a 64 KiB smem window,
+// counted with red.shared (no return value, no wrap test: a CTA counts
+// < 2^32 samples); the rest go to the packed histogram (plain layout).
+// Packed pairs put neighbouring values -- a smooth image's warp samples --
+// on the same word with different increments, which the atomic unit
+// serialises: C3 ramp12's count 0.481 -> 0.390 ms in tools/hist_probe.cu
+// (profiles/r2/hist_probe_window.txt).  fold_window() moves the window into
+// the packed histogram before the partial flush (the window's packed
+// halves are untouched: every in-window sample went to the window).
+struct WindowCounter {
+  uint32_t* bins;
+  uint32_t* overflow;
+  uint32_t* win;
+  uint32_t lo;  // even
+  __device__ __forceinline__ void one(uint32_t v) const {
+    const uint32_t d = v - lo;
+    if (d < kWinBins) atomicAdd(win + d, 1u);
+    else count_one<0>(bins, overflow, v);
+  }
+  __device__ __forceinline__ void vec(uint4 q) const {
+    one(q.x & 0xFFFFu); one(q.x >> 16); one(q.y & 0xFFFFu); one(q.y >> 16);
+    one(q.z & 0xFFFFu); one(q.z >> 16); one(q.w & 0xFFFFu); one(q.w >> 16);
+  }
+  __device__ __forceinline__ void pair(uint4 a, uint4 b) const {
+    // per u16 half v - lo (wrapping below lo): in the window iff < 0x4000
+    const uint32_t l2 = lo * 0x10001u;
+    const uint32_t d[8] = {__vsub2(a.x, l2), __vsub2(a.y, l2), __vsub2(a.z, l2), __vsub2(a.w, l2),
+                           __vsub2(b.x, l2), __vsub2(b.y, l2), __vsub2(b.z, l2), __vsub2(b.w, l2)};
+    static_assert(kWinBins == 0x4000, "window test");
+    const uint32_t any = d[0] | d[1] | d[2] | d[3] | d[4] | d[5] | d[6] | d[7];
+    if (__all_sync(__activemask(), (any & 0xC000C000u) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        atomicAdd(win + (d[j] & 0xFFFFu), 1u);
+        atomicAdd(win + (d[j] >> 16), 1u);
+      }
+    } else {
+      vec(a);
+      vec(b);
+    }
+  }
+};
+
+// Window counts into the packed histogram (all threads, after the count
+// pass's barrier; a barrier must follow): word (lo + 2i) / 2 gets the low 16
+// bits of both counts, the rest of a count above 65535 goes to the overflow
+// counters the merge adds back.
+__device__ __forceinline__ void fold_window(uint32_t* bins, uint32_t* overflow, const uint32_t* win,
+                                            uint32_t lo) {
+  for (uint32_t i = threadIdx.x; i < kWinBins / 2; i += kThreads) {
+    const uint2 c = reinterpret_cast<const uint2*>(win)[i];
+    const uint32_t v0 = lo + 2 * i;
+    bins[v0 >> 1] = (c.x & 0xFFFFu) | (c.y << 16);
+    if (c.x > 0xFFFFu) atomicAdd(&overflow[v0], c.x & 0xFFFF0000u);
+    if (c.y > 0xFFFFu) atomicAdd(&overflow[v0 + 1], c.y & 0xFFFF0000u);
+  }
+}
+
 // Per-launch choices from a fixed sample -- 256 pairs of adjacent samples
 // spread over the image, the same in every CTA:
 //   bits 0-1  smem layout: 0 plain; 1 / 2 swizzled when the OR of the
@@ -311,12 +394,15 @@ __device__ __forceinline__ void count_pair(uint32_t* bins, uint32_t* overflow, u
 //   bit 3  smooth data: >= 1/2 of the pairs differ by < 64 -> worth coding
 //          the residual plane (fused_kernel); noise-like images skip its
 //          per-block test, which would mark every block raw (~3% on them).
+// and (`wlo`, optional) the count pass's u32 window (WindowCounter): its
+// first value, even, when the sampled values span less than kWinBins - 2048
+// (the window centred on them), else kNoWindow.
 // Warp 0 computes the flags into *flags; the caller's next __syncthreads
 // publishes them.  They change where and how counts are added, never what.
 __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uint64_t n,
-                                              uint32_t* flags) {
+                                              uint32_t* flags, uint32_t* wlo = nullptr) {
   if (threadIdx.x >= 32) return;
-  uint32_t o = 0, eq = 0, near = 0;
+  uint32_t o = 0, eq = 0, near = 0, mn = 0xFFFFu, mx = 0;
   if (n >= 2) {
     // 8 pairs per lane, all 16 loads in flight at once (this runs while
     // the other warps zero the histogram, and C1's whole kernel is ~40 us)
@@ -334,6 +420,8 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
       o |= a[k] | b[k];
       eq += a[k] == b[k];
       near += (a[k] > b[k] ? a[k] - b[k] : b[k] - a[k]) < 64u;
+      mn = min(mn, min(a[k], b[k]));
+      mx = max(mx, max(a[k], b[k]));
     }
   } else if (n == 1 && threadIdx.x == 0) {
     o = img[0];
@@ -341,10 +429,21 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
   o = __reduce_or_sync(0xFFFFFFFFu, o);
   eq = __reduce_add_sync(0xFFFFFFFFu, eq);
   near = __reduce_add_sync(0xFFFFFFFFu, near);
+  mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
   if (threadIdx.x == 0) {
     const uint32_t tz = o == 0 ? 32u : static_cast<uint32_t>(__ffs(o) - 1);
     const uint32_t layout = (n == 0 || tz < 3) ? 0u : (tz <= 6 ? 1u : 2u);
     *flags = layout | (eq >= 32 ? 4u : 0u) | (near >= 128 ? 8u : 0u);
+    if (wlo != nullptr) {
+      uint32_t lo = kNoWindow;
+      if (n >= 2 && mx >= mn && mx - mn <= kWinBins - 2048) {
+        const uint32_t pad = (kWinBins - (mx - mn)) / 2;
+        lo = mn > pad ? mn - pad : 0u;
+        lo = min(lo, 65536u - kWinBins) & ~1u;
+      }
+      *wlo = lo;
+    }
   }
 }
 
@@ -390,18 +489,16 @@ __device__ __forceinline__ void stage_lut(uint4* smem, const std::uint16_t* lut_
 // Histogram of img[0, n) into the packed smem bins; CTA `cta` of `ctas`
 // (grid-stride over 128-bit vectors, two-vector software pipeline: the next
 // stage's loads are in flight while this stage's 16 samples are counted).
-template <int kSwz, bool kFew>
-__device__ __forceinline__ void count_image(const std::uint16_t* img,
-                                            std::uint64_t n, int cta, int ctas,
-                                            uint32_t* bins, uint32_t* overflow) {
+template <class Ctr>
+__device__ __forceinline__ void count_image(const std::uint16_t* img, std::uint64_t n, int cta,
+                                            int ctas, const Ctr& ctr) {
   const std::uint64_t head = head_len(img, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t tail0 = head + (nvec << 3);
   if (cta == 0)
-    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one<kSwz>(bins, overflow, img[i]);
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) ctr.one(img[i]);
   if (cta == ctas - 1)
-    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
-      count_one<kSwz>(bins, overflow, img[i]);
+    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads) ctr.one(img[i]);
   const uint4* body = reinterpret_cast<const uint4*>(img + head);
   const std::uint64_t stride = static_cast<std::uint64_t>(ctas) * kThreads;
   std::uint64_t i = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
@@ -418,20 +515,13 @@ __device__ __forceinline__ void count_image(const std::uint16_t* img,
       nq[0] = ld_stream(body + nx);
       nq[1] = ld_stream(body + nx + stride);
     }
-    if constexpr (kFew) {
-      count_pair<kSwz>(bins, overflow, q[0], q[1]);
-    } else {
-      count_pair_plain<kSwz>(bins, overflow, q[0], q[1]);
-    }
+    ctr.pair(q[0], q[1]);
     q[0] = nq[0];
     q[1] = nq[1];
     i = nx;
     have = nhave;
   }
-  for (; i < nvec; i += stride) {
-    if constexpr (kFew) count_vec<kSwz>(bins, overflow, ld_stream(body + i));
-    else count_vec_plain<kSwz>(bins, overflow, ld_stream(body + i));
-  }
+  for (; i < nvec; i += stride) ctr.vec(ld_stream(body + i));
 }
 
 // out = LUT[in] over [0, n) with the LUT in smem; CTA `cta` of `ctas`.
@@ -560,23 +650,21 @@ __device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk
 // next block's two loads in flight while this one is coded and counted),
 // coding each block into the plane; the < 64 vectors past the last whole
 // block go to the last CTA, uncoded.
-template <int kSwz, bool kFew>
+template <class Ctr>
 __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std::uint64_t n,
-                                                  int cta, int ctas, uint32_t* bins,
-                                                  uint32_t* overflow, uint32_t* pbase,
-                                                  uint4* pres) {
+                                                  int cta, int ctas, const Ctr& ctr,
+                                                  uint32_t* pbase, uint4* pres) {
   const std::uint64_t head = head_len(img, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t nblk = nvec >> 6;
   const std::uint64_t tail0 = head + (nvec << 3);
   const uint4* body = reinterpret_cast<const uint4*>(img + head);
   if (cta == 0)
-    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) count_one<kSwz>(bins, overflow, img[i]);
+    for (std::uint64_t i = threadIdx.x; i < head; i += kThreads) ctr.one(img[i]);
   if (cta == ctas - 1) {
-    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads)
-      count_one<kSwz>(bins, overflow, img[i]);
+    for (std::uint64_t i = tail0 + threadIdx.x; i < n; i += kThreads) ctr.one(img[i]);
     for (std::uint64_t v = (nblk << 6) + threadIdx.x; v < nvec; v += kThreads)
-      count_vec_plain<kSwz>(bins, overflow, ld_stream(body + v));
+      ctr.vec(ld_stream(body + v));
   }
   const uint32_t lane = threadIdx.x & 31u;
   const std::uint64_t W = static_cast<std::uint64_t>(ctas) * (kThreads / 32);
@@ -589,11 +677,7 @@ __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std:
   };
   auto work = [&](std::uint64_t blk, uint4 x0, uint4 x1) {
     code_block(x0, x1, blk, lane, pbase, pres);
-    if constexpr (kFew) {
-      count_pair<kSwz>(bins, overflow, x0, x1);
-    } else {
-      count_pair_plain<kSwz>(bins, overflow, x0, x1);
-    }
+    ctr.pair(x0, x1);
   };
   if (b < nblk) load(b, qa0, qa1);  // warp-uniform conditions throughout
   while (b < nblk) {
@@ -916,31 +1000,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(0);
   const bool count = stages & kCount;
   // smem layout of this launch (the same in every CTA: a fixed sample of img)
-  __shared__ uint32_t s_swz;
-  if ((stages & (kCount | kApply)) != 0) sample_layout(img, n, &s_swz);
+  __shared__ uint32_t s_swz, s_wlo;
+  if ((stages & (kCount | kApply)) != 0) sample_layout(img, n, &s_swz, &s_wlo);
   if (!count) __syncthreads();  // else published by the zeroing's barrier
   // ---- phase 1: per-CTA histograms
+  uint32_t* win = bins + kWords;  // the u32 window after the packed bins
   if (count && static_cast<int>(blockIdx.x) < nparts) {
-    for (int i = t; i < kWords / 4; i += kThreads) smem_u4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = t; i < (kWords + static_cast<int>(kWinBins)) / 4; i += kThreads)
+      smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    if (plane != nullptr && (s_swz & 8u) != 0) {
-      switch (s_swz & 7u) {
-        case 0: count_image_coded<0, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-        case 1: count_image_coded<1, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-        case 2: count_image_coded<2, false>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-        case 4: count_image_coded<0, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-        case 5: count_image_coded<1, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-        default: count_image_coded<2, true>(img, n, blockIdx.x, nparts, bins, overflow, pbase, pres); break;
-      }
-    } else {
-      switch (s_swz & 7u) {
-        case 0: count_image<0, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-        case 1: count_image<1, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-        case 2: count_image<2, false>(img, n, blockIdx.x, nparts, bins, overflow); break;
-        case 4: count_image<0, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-        case 5: count_image<1, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-        default: count_image<2, true>(img, n, blockIdx.x, nparts, bins, overflow); break;
-      }
+    const bool coded = plane != nullptr && (s_swz & 8u) != 0;
+    auto run = [&](const auto& ctr) {
+      if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres);
+      else count_image(img, n, blockIdx.x, nparts, ctr);
+    };
+    switch (s_swz & 7u) {
+      case 0:
+        if (s_wlo != kNoWindow) run(WindowCounter{bins, overflow, win, s_wlo});
+        else run(PlainCounter<0>{bins, overflow});
+        break;
+      case 1: run(PlainCounter<1>{bins, overflow}); break;
+      case 2: run(PlainCounter<2>{bins, overflow}); break;
+      case 4: run(FewCounter<0>{bins, overflow}); break;
+      case 5: run(FewCounter<1>{bins, overflow}); break;
+      default: run(FewCounter<2>{bins, overflow}); break;
+    }
+    if ((s_swz & 7u) == 0 && s_wlo != kNoWindow) {
+      __syncthreads();
+      fold_window(bins, overflow, win, s_wlo);
     }
     __syncthreads();
     LUT_STAMP(1);
