@@ -9,8 +9,10 @@
 // Kernels (see DESIGN.md for the roofline of each):
 //   fused_kernel    the equalize path, one cooperative launch, phases
 //                   selected per call: histogram (1 CTA/SM, 128 KiB smem of
-//                   packed u16 pairs, 128-bit streaming loads, 2 B/px) ->
-//                   partial merge -> LUT -> apply (4 B/px).
+//                   packed u16 pairs + a 64 KiB u32 window for narrow data,
+//                   128-bit streaming loads, 2 B/px; from 2^25 samples it
+//                   also writes the 1 B/px residual plane) -> partial merge
+//                   -> LUT -> apply (4 B/px, or 1 + 2 B/px from the plane).
 //   stretch_fused_kernel  LUT_CORRECT stretch, one cooperative launch:
 //                   min/max (2 B/px) -> grid sync -> per-CTA LUT in smem ->
 //                   apply (4 B/px).
