@@ -110,3 +110,20 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(G.GpcxError) as e:
         G.run("LUT_CORRECT", "rows=4,cols=4", img)
     assert e.value.code == "TaskFailed"
+
+
+def test_lut_workspace_size_includes_the_residual_plane():
+    """gpcx_lut_workspace_size(n): the fixed part below 2^25 samples; from
+    2^25 on plus the residual plane (u32 base per 512-sample block, 256-byte
+    rounded, and 512 residual bytes per block -- DESIGN.md §4)."""
+    def size(n):
+        nb = C.c_uint64(0)
+        assert G.lib.gpcx_lut_workspace_size(n, C.byref(nb)) == 0
+        return nb.value
+    fixed = size(1)
+    assert size((1 << 25) - 1) == fixed
+    for n in (1 << 25, (1 << 25) + 511, 1 << 30, (1 << 32) - 1):
+        blocks = n >> 9
+        assert size(n) == fixed + ((blocks * 4 + 255) & ~255) + blocks * 512, n
+    nb = C.c_uint64(0)
+    assert G.lib.gpcx_lut_workspace_size(1 << 32, C.byref(nb)) != 0  # n must fit u32
