@@ -1016,18 +1016,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres);
       else count_image(img, n, blockIdx.x, nparts, ctr);
     };
-    switch (s_swz & 7u) {
-      case 0:
-        if (s_wlo != kNoWindow) run(WindowCounter{bins, overflow, win, s_wlo});
-        else run(PlainCounter<0>{bins, overflow});
-        break;
+    // the window serves repetitive data too (flat / few-level images within
+    // its span): red.shared of many lanes on one u32 counter runs at the
+    // HBM rate (tools/hist_probe.cu mode 2), with no warp-combining probe
+    const bool windowed = (s_swz & 3u) == 0 && s_wlo != kNoWindow;
+    switch (windowed ? 0xFFu : (s_swz & 7u)) {
+      case 0xFF: run(WindowCounter{bins, overflow, win, s_wlo}); break;
+      case 0: run(PlainCounter<0>{bins, overflow}); break;
       case 1: run(PlainCounter<1>{bins, overflow}); break;
       case 2: run(PlainCounter<2>{bins, overflow}); break;
       case 4: run(FewCounter<0>{bins, overflow}); break;
       case 5: run(FewCounter<1>{bins, overflow}); break;
       default: run(FewCounter<2>{bins, overflow}); break;
     }
-    if ((s_swz & 7u) == 0 && s_wlo != kNoWindow) {
+    if (windowed) {
       __syncthreads();
       fold_window(bins, overflow, win, s_wlo);
     }

@@ -399,17 +399,22 @@ def test_swizzled_and_flat_counter_wraps(gpu):
 
 
 @pytest.mark.parametrize("variant", ["plain", "plain_swizzled", "few", "few_swizzled", "few_random",
-                                     "few_random_swizzled"])
+                                     "few_random_swizzled", "plain_wide", "few_wide",
+                                     "few_random_wide"])
 def test_counter_wraps_every_count_variant(gpu, variant):
-    """Each of the four count-pass variants (smem layout plain / swizzled x
-    repetitive-data probe off / on, picked per launch from a fixed sample)
-    with > 65535 samples of a value per CTA, so the packed u16 halves wrap."""
+    """Each count-pass variant (smem layout plain / swizzled x repetitive-
+    data probe off / on x the u32 window for narrow data, picked per launch
+    from a fixed sample) with > 65535 samples of a value per CTA, so the
+    packed u16 halves wrap (or, in the window, the fold books counts above
+    16 bits into the overflow counters).  [1000, 1001]: narrow -> the
+    window; [1000, 40001]: too wide for it -> the packed plain / few paths."""
     torch, D = _dev()
     n = 24_000_007  # 2 values over 148 CTAs: ~81K samples of each per CTA
     # swizzle strength from the trailing zeros: 0x3008 -> 3 (layout 1),
     # 0x3100 -> 8 (layout 2)
     base = np.array([0x3000, 0x3100] if variant == "few_random_swizzled" else
-                    [0x3000, 0x3008] if "swizzled" in variant else [1000, 1001], dtype=np.uint16)
+                    [0x3000, 0x3008] if "swizzled" in variant else
+                    [1000, 40001] if "wide" in variant else [1000, 1001], dtype=np.uint16)
     if variant.startswith("plain"):
         vals = base[np.arange(n) % 2]               # adjacent samples always differ
     elif "random" in variant:                        # binary noise: the min/max path

@@ -2,7 +2,7 @@
 // stamps of thread 0 of every CTA; design exploration, not product code).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DGPCX_LUT_TRACE \
 //        -o tools/fused_trace tools/fused_trace.cu paper_1505_05655_b200/csrc/status.cpp
-//   ./tools/fused_trace [rows cols [r|u]]   (bench.py's ramp12 / uniform16 scenes)   (GPCX_LUT_PLANE=0: no residual plane)
+//   ./tools/fused_trace [rows cols [r|u]]   (bench.py's ramp12 / uniform16 scenes, c: constant)   (GPCX_LUT_PLANE=0: no residual plane)
 #include "../paper_1505_05655_b200/csrc/lut.cu"
 #include "../paper_1505_05655_b200/csrc/synth.cu"  // the bench's ramp12 / uniform16 scenes
 
@@ -15,10 +15,15 @@ void note_cuda_error(cudaError_t, const char*) {}
 #include <cstdlib>
 #include <vector>
 
+__global__ void fill_kernel(std::uint16_t* p, std::uint64_t n, std::uint16_t v) {
+  for (std::uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 1024ull * 256) p[i] = v;
+}
+
 int main(int argc, char** argv) {
   const std::uint64_t rows = argc > 2 ? std::strtoull(argv[1], nullptr, 10) : 4096;
   const std::uint64_t cols = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 4096;
-  const int kind = argc > 3 && argv[3][0] == 'u' ? 1 : 0;  // r: ramp12, u: uniform16 (seed 0x5eed)
+  const char kc = argc > 3 ? argv[3][0] : 'r';
+  const int kind = kc == 'u' ? 1 : 0;  // r: ramp12, u: uniform16 (seed 0x5eed), c: constant 1234
   const std::uint64_t n = rows * cols;
   std::uint16_t *img, *out, *lut;
   void* ws;
@@ -35,6 +40,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&trace, sms * 16 * 8);
   cudaMemcpyToSymbol(gpcx::lut::g_lut_trace, &trace, sizeof(trace));
   gpcx::synth::launch_image(kind, 0x5EED, rows, cols, 0, rows, img, nullptr);
+  if (kc == 'c') fill_kernel<<<1024, 256>>>(img, n, 1234);
   cudaDeviceSynchronize();
   char* flush;
   cudaMalloc(&flush, 512 << 20);
