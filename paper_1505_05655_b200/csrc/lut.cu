@@ -62,9 +62,11 @@ constexpr int kSmemHist = kWords * 4 + 65536;  // 128 KiB packed bins + the 64 K
 constexpr int kSmemLut = kBins * 2;    // 128 KiB
 constexpr int kUnroll = 4;
 
-// u32 work counter of the apply pass's dynamic tail (apply_image), in the
-// unused end of the min/max slot area; reset before the grid sync that
-// precedes every cooperative apply.
+// u32 work counters of the apply pass's dynamic tail (apply_image) and of
+// the coded count pass's (count_tail_coded, the next word), in the unused
+// end of the min/max slot area; the apply's is reset before the grid sync
+// that precedes every cooperative apply, the count's after the grid sync
+// that ends the count pass (so it is zero at the next launch).
 constexpr std::uint64_t kTailOff = kMinMaxOff + 4 * 1024 - 64;
 static_assert(kMaxParts * 8 <= 4 * 1024 - 64, "min/max slot area");
 
@@ -652,10 +654,47 @@ __device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk
 // next block's two loads in flight while this one is coded and counted),
 // coding each block into the plane; the < 64 vectors past the last whole
 // block go to the last CTA, uncoded.
+// The coded count pass's last blocks, 8-block chunks taken warp by warp
+// from a counter (the next chunk's index requested while this one is
+// counted).  Out of line so its registers do not crowd the main loop.
+template <class Ctr>
+__device__ __noinline__ void count_tail_coded(const uint4* body, std::uint64_t static_end,
+                                              std::uint32_t tail_chunks, std::uint32_t* ctail,
+                                              Ctr ctr, uint32_t* pbase, uint4* pres) {
+  constexpr std::uint64_t kWChunk = 8;
+  const uint32_t lane = threadIdx.x & 31u;
+  std::uint32_t c = 0;
+  if (lane == 0) c = atomicAdd(ctail, 1u);
+  c = __shfl_sync(0xFFFFFFFFu, c, 0);
+  uint4 qa0, qa1, qb0, qb1;
+  while (c < tail_chunks) {
+    std::uint32_t nc = 0;
+    if (lane == 0) nc = atomicAdd(ctail, 1u);  // consumed after this chunk
+    const std::uint64_t b0 = static_end + static_cast<std::uint64_t>(c) * kWChunk;
+    qa0 = ld_stream(body + (b0 << 6) + lane);
+    qa1 = ld_stream(body + (b0 << 6) + 32 + lane);
+#pragma unroll 1
+    for (std::uint64_t j = 0; j < kWChunk; j += 2) {
+      qb0 = ld_stream(body + ((b0 + j + 1) << 6) + lane);
+      qb1 = ld_stream(body + ((b0 + j + 1) << 6) + 32 + lane);
+      code_block(qa0, qa1, b0 + j, lane, pbase, pres);
+      ctr.pair(qa0, qa1);
+      if (j + 2 < kWChunk) {
+        qa0 = ld_stream(body + ((b0 + j + 2) << 6) + lane);
+        qa1 = ld_stream(body + ((b0 + j + 2) << 6) + 32 + lane);
+      }
+      code_block(qb0, qb1, b0 + j + 1, lane, pbase, pres);
+      ctr.pair(qb0, qb1);
+    }
+    c = __shfl_sync(0xFFFFFFFFu, nc, 0);
+  }
+}
+
 template <class Ctr>
 __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std::uint64_t n,
                                                   int cta, int ctas, const Ctr& ctr,
-                                                  uint32_t* pbase, uint4* pres) {
+                                                  uint32_t* pbase, uint4* pres,
+                                                  std::uint32_t* ctail) {
   const std::uint64_t head = head_len(img, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t nblk = nvec >> 6;
@@ -681,16 +720,21 @@ __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std:
     code_block(x0, x1, blk, lane, pbase, pres);
     ctr.pair(x0, x1);
   };
-  if (b < nblk) load(b, qa0, qa1);  // warp-uniform conditions throughout
-  while (b < nblk) {
-    if (b + W < nblk) load(b + W, qb0, qb1);
+  // the last ~3% of the blocks are handed out dynamically (count_tail_coded):
+  // SMs do not count at identical rates (a ~20 us first-to-last spread)
+  const std::uint32_t tail_chunks = static_cast<std::uint32_t>(nblk / (32 * 8));
+  const std::uint64_t static_end = nblk - static_cast<std::uint64_t>(tail_chunks) * 8;
+  if (b < static_end) load(b, qa0, qa1);  // warp-uniform conditions throughout
+  while (b < static_end) {
+    if (b + W < static_end) load(b + W, qb0, qb1);
     work(b, qa0, qa1);
     b += W;
-    if (b >= nblk) break;
-    if (b + W < nblk) load(b + W, qa0, qa1);
+    if (b >= static_end) break;
+    if (b + W < static_end) load(b + W, qa0, qa1);
     work(b, qb0, qb1);
     b += W;
   }
+  if (tail_chunks != 0) count_tail_coded(body, static_end, tail_chunks, ctail, ctr, pbase, pres);
 }
 
 // Block vectors as loaded for the apply: a narrow block's residuals (r0,
@@ -1013,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     const bool coded = plane != nullptr && (s_swz & 8u) != 0;
     auto run = [&](const auto& ctr) {
-      if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres);
+      if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres, tail + 1);
       else count_image(img, n, blockIdx.x, nparts, ctr);
     };
     // the window serves repetitive data too (flat / few-level images within
@@ -1040,6 +1084,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   LUT_STAMP(2);
   if (count) grid.sync();
+  // the coded count pass's chunk counter, zero again for the next launch
+  if (count && blockIdx.x == 0 && t == 0) tail[1] = 0;
   LUT_STAMP(3);
   const uint32_t layout = s_swz & 3u;  // published by a barrier above (read only with img)
 

@@ -77,6 +77,11 @@ int main(int argc, char** argv) {
       if (cnt) std::printf("  %-10s min %7.2f  avg %7.2f  max %7.2f us  (%d CTAs)\n", names[k], mn,
                            sum / cnt, mx, cnt);
     }
+    if (rep == 3 && std::getenv("TRACE_CTAS") != nullptr) {  // per-CTA end of the count pass
+      std::printf("  counted per CTA (us):");
+      for (int c = 0; c < sms; ++c) std::printf(" %d:%.1f", c, (t[c * 16 + 1] - t0) * 1e-3);
+      std::printf("\n");
+    }
   }
   return 0;
 }
