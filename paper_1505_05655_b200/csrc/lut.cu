@@ -319,7 +319,7 @@ struct PlainCounter {  // packed u16 pairs, returning atomics, wrap test
   }
 };
 template <int kSwz>
-struct FewCounter {  // repetitive data: warp-combined counts (count_vec_few)
+struct FewCounter {  // repetitive data too wide for the window: warp-combined counts
   uint32_t* bins;
   uint32_t* overflow;
   __device__ __forceinline__ void one(uint32_t v) const { count_one<kSwz>(bins, overflow, v); }
@@ -335,7 +335,9 @@ struct FewCounter {  // repetitive data: warp-combined counts (count_vec_few)
 // Packed pairs put neighbouring values -- a smooth image's warp samples --
 // on the same word with different increments, which the atomic unit
 // serialises: C3 ramp12's count 0.481 -> 0.390 ms in tools/hist_probe.cu
-// (profiles/r2/hist_probe_window.txt).  fold_window() moves the window into
+// (profiles/r2/hist_probe_window.txt); flat / few-level data in the window
+// is fast too (many lanes' red on one counter run at the HBM rate).
+// fold_window() moves the window into
 // the packed histogram before the partial flush (the window's packed
 // halves are untouched: every in-window sample went to the window).
 struct WindowCounter {
