@@ -340,32 +340,37 @@ struct FewCounter {  // repetitive data too wide for the window: warp-combined c
 // fold_window() moves the window into
 // the packed histogram before the partial flush (the window's packed
 // halves are untouched: every in-window sample went to the window).
+template <int kSwz>
 struct WindowCounter {
   uint32_t* bins;
   uint32_t* overflow;
   uint32_t* win;
-  uint32_t lo;  // even
+  uint32_t lo;  // even; 0 when shifted
+  uint32_t sh;  // 0, or the trailing zero bits of MSB-aligned data (lo 0)
+  // per u16 half d = v - lo: in the window iff (d & reject) == 0
+  __device__ __forceinline__ uint32_t reject() const { return sh == 0 ? 0xC000u : (1u << sh) - 1u; }
   __device__ __forceinline__ void one(uint32_t v) const {
-    const uint32_t d = v - lo;
-    if (d < kWinBins) atomicAdd(win + d, 1u);
-    else count_one<0>(bins, overflow, v);
+    const uint32_t d = (v - lo) & 0xFFFFu;
+    if (v >= lo && (d & reject()) == 0) atomicAdd(win + (d >> sh), 1u);
+    else count_one<kSwz>(bins, overflow, v);
   }
   __device__ __forceinline__ void vec(uint4 q) const {
     one(q.x & 0xFFFFu); one(q.x >> 16); one(q.y & 0xFFFFu); one(q.y >> 16);
     one(q.z & 0xFFFFu); one(q.z >> 16); one(q.w & 0xFFFFu); one(q.w >> 16);
   }
   __device__ __forceinline__ void pair(uint4 a, uint4 b) const {
-    // per u16 half v - lo (wrapping below lo): in the window iff < 0x4000
+    // per u16 half v - lo (wrapping below lo: a narrow window's test bits
+    // 14-15 catch it; a shifted window has lo 0)
     const uint32_t l2 = lo * 0x10001u;
     const uint32_t d[8] = {__vsub2(a.x, l2), __vsub2(a.y, l2), __vsub2(a.z, l2), __vsub2(a.w, l2),
                            __vsub2(b.x, l2), __vsub2(b.y, l2), __vsub2(b.z, l2), __vsub2(b.w, l2)};
     static_assert(kWinBins == 0x4000, "window test");
     const uint32_t any = d[0] | d[1] | d[2] | d[3] | d[4] | d[5] | d[6] | d[7];
-    if (__all_sync(__activemask(), (any & 0xC000C000u) == 0)) {
+    if (__all_sync(__activemask(), (any & (reject() * 0x10001u)) == 0)) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        atomicAdd(win + (d[j] & 0xFFFFu), 1u);
-        atomicAdd(win + (d[j] >> 16), 1u);
+        atomicAdd(win + ((d[j] & 0xFFFFu) >> sh), 1u);
+        atomicAdd(win + (d[j] >> (16 + sh)), 1u);
       }
     } else {
       vec(a);
@@ -375,17 +380,30 @@ struct WindowCounter {
 };
 
 // Window counts into the packed histogram (all threads, after the count
-// pass's barrier; a barrier must follow): word (lo + 2i) / 2 gets the low 16
-// bits of both counts, the rest of a count above 65535 goes to the overflow
-// counters the merge adds back.
+// pass's barrier; a barrier must follow): counter i is value lo + (i << sh);
+// its packed half gets the low 16 bits (the half was never touched: every
+// sample of that value went to the window), the rest of a count above
+// 65535 goes to the overflow counters the merge adds back.  Narrow window:
+// counters 2i, 2i + 1 fill one word; shifted: one even value per word.
+template <int kSwz>
 __device__ __forceinline__ void fold_window(uint32_t* bins, uint32_t* overflow, const uint32_t* win,
-                                            uint32_t lo) {
-  for (uint32_t i = threadIdx.x; i < kWinBins / 2; i += kThreads) {
-    const uint2 c = reinterpret_cast<const uint2*>(win)[i];
-    const uint32_t v0 = lo + 2 * i;
-    bins[v0 >> 1] = (c.x & 0xFFFFu) | (c.y << 16);
-    if (c.x > 0xFFFFu) atomicAdd(&overflow[v0], c.x & 0xFFFF0000u);
-    if (c.y > 0xFFFFu) atomicAdd(&overflow[v0 + 1], c.y & 0xFFFF0000u);
+                                            uint32_t lo, uint32_t sh) {
+  if (sh == 0) {
+    for (uint32_t i = threadIdx.x; i < kWinBins / 2; i += kThreads) {
+      const uint2 c = reinterpret_cast<const uint2*>(win)[i];
+      const uint32_t v0 = lo + 2 * i;
+      bins[phys_word<kSwz>(v0 >> 1)] += (c.x & 0xFFFFu) | (c.y << 16);
+      if (c.x > 0xFFFFu) atomicAdd(&overflow[v0], c.x & 0xFFFF0000u);
+      if (c.y > 0xFFFFu) atomicAdd(&overflow[v0 + 1], c.y & 0xFFFF0000u);
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < kWinBins && (i << sh) <= 0xFFFFu; i += kThreads) {
+      const uint32_t c = win[i];
+      if (c == 0) continue;
+      const uint32_t v = i << sh;  // even: the low half of its word
+      bins[phys_word<kSwz>(v >> 1)] += c & 0xFFFFu;
+      if (c > 0xFFFFu) atomicAdd(&overflow[v], c & 0xFFFF0000u);
+    }
   }
 }
 
@@ -400,20 +418,27 @@ __device__ __forceinline__ void fold_window(uint32_t* bins, uint32_t* overflow, 
 //   bit 3  smooth data: >= 1/2 of the pairs differ by < 64 -> worth coding
 //          the residual plane (fused_kernel); noise-like images skip its
 //          per-block test, which would mark every block raw (~3% on them).
-// and (`wlo`, optional) the count pass's u32 window (WindowCounter): its
-// first value, even, when the sampled values span less than kWinBins - 2048
-// (the window centred on them), else kNoWindow.
+//          MSB-aligned data (>= 2 trailing zero bits) counts as smooth when
+//          the pairs differ by < 64 steps of 2^tz; bits 8-11 then hold the
+//          plane's residual shift min(tz, 8).
+// and (`wlo`, `wsh`, optional) the count pass's u32 window (WindowCounter):
+// either narrow data (plain layout, sampled values spanning less than
+// kWinBins - 2048): first value `wlo` (even, the window centred on them),
+// shift 0; or MSB-aligned data (>= 2 trailing zero bits): wlo 0 and shift
+// = the trailing zeros, counter v >> shift for every v with those bits
+// clear (all of [0, 65536)); else kNoWindow.
 // Warp 0 computes the flags into *flags; the caller's next __syncthreads
 // publishes them.  They change where and how counts are added, never what.
 __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uint64_t n,
-                                              uint32_t* flags, uint32_t* wlo = nullptr) {
+                                              uint32_t* flags, uint32_t* wlo = nullptr,
+                                              uint32_t* wsh = nullptr) {
   if (threadIdx.x >= 32) return;
   uint32_t o = 0, eq = 0, near = 0, mn = 0xFFFFu, mx = 0;
+  uint32_t a[8] = {}, b[8] = {};
   if (n >= 2) {
     // 8 pairs per lane, all 16 loads in flight at once (this runs while
     // the other warps zero the histogram, and C1's whole kernel is ~40 us)
     const double step = static_cast<double>(n - 2) / 255.0;
-    uint32_t a[8], b[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const std::uint64_t p =
@@ -437,18 +462,36 @@ __device__ __forceinline__ void sample_layout(const std::uint16_t* img, std::uin
   near = __reduce_add_sync(0xFFFFFFFFu, near);
   mn = __reduce_min_sync(0xFFFFFFFFu, mn);
   mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  const uint32_t tz = o == 0 ? 32u : static_cast<uint32_t>(__ffs(o) - 1);
+  // smooth in units of the data's step (MSB-aligned data: 2^tz)
+  const uint32_t s8 = min(tz, 8u);
+  uint32_t nearsh = 0;
+  if (n >= 2) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nearsh += ((a[k] > b[k] ? a[k] - b[k] : b[k] - a[k]) >> s8) < 64u;
+  }
+  nearsh = __reduce_add_sync(0xFFFFFFFFu, nearsh);
   if (threadIdx.x == 0) {
-    const uint32_t tz = o == 0 ? 32u : static_cast<uint32_t>(__ffs(o) - 1);
     const uint32_t layout = (n == 0 || tz < 3) ? 0u : (tz <= 6 ? 1u : 2u);
-    *flags = layout | (eq >= 32 ? 4u : 0u) | (near >= 128 ? 8u : 0u);
+    // the residual plane: smooth data (raw units, or steps of 2^tz up to 2^8)
+    uint32_t plane = 0;
+    if (near >= 128) plane = 8u;
+    else if (n >= 2 && tz >= 2 && tz < 32 && nearsh >= 128) plane = 8u | (s8 << 8);
+    *flags = layout | (eq >= 32 ? 4u : 0u) | plane;
     if (wlo != nullptr) {
-      uint32_t lo = kNoWindow;
-      if (n >= 2 && mx >= mn && mx - mn <= kWinBins - 2048) {
+      uint32_t lo = kNoWindow, sh = 0;
+      if (n >= 2 && tz >= 2 && tz < 32 && (tz >= 7 || nearsh >= 128)) {
+        // MSB-aligned data, smooth or with few levels: counter v >> tz (random
+        // data with 1024+ levels runs faster on the swizzled packed bins)
+        lo = 0;
+        sh = min(tz, 15u);
+      } else if (n >= 2 && layout == 0 && mx >= mn && mx - mn <= kWinBins - 2048) {
         const uint32_t pad = (kWinBins - (mx - mn)) / 2;
         lo = mn > pad ? mn - pad : 0u;
         lo = min(lo, 65536u - kWinBins) & ~1u;
       }
       *wlo = lo;
+      *wsh = sh;
     }
   }
 }
@@ -637,32 +680,34 @@ __device__ __forceinline__ uint4 ld_plane(const uint4* p) {
 // tree (the count pass is issue-sensitive: +35 instructions per block of a
 // redux min/max version cost ~75 us at C3).
 __device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk, uint32_t lane,
-                                           uint32_t* pbase, uint4* pres) {
+                                           uint32_t* pbase, uint4* pres, uint32_t sh) {
+  // sh > 0 (MSB-aligned data, steps of 2^sh): window [base, base + 256 << sh),
+  // residual (v - base) >> sh; a sample off the step grid rejects the block
   const uint32_t f = __shfl_sync(0xFFFFFFFFu, q0.x, 0) & 0xFFFFu;
-  const uint32_t base = min(max(f, 128u) - 128u, 65280u);
+  const uint32_t half = 128u << sh, lim = 65536u - (256u << sh);
+  const uint32_t base = min(max(f, half) - half, lim);
   const uint32_t b2 = base * 0x10001u;
   const uint4 d0 = make_uint4(q0.x - b2, q0.y - b2, q0.z - b2, q0.w - b2);
   const uint4 d1 = make_uint4(q1.x - b2, q1.y - b2, q1.z - b2, q1.w - b2);
   const uint32_t any = d0.x | d0.y | d0.z | d0.w | d1.x | d1.y | d1.z | d1.w;
-  const bool narrow = __all_sync(0xFFFFFFFFu, (any & 0xFF00FF00u) == 0);
-  if (narrow)
+  const uint32_t rej = (0xFFFFu & ~(0xFFu << sh)) * 0x10001u;
+  const bool narrow = __all_sync(0xFFFFFFFFu, (any & rej) == 0);
+  if (narrow) {
+    auto r = [sh](uint32_t d) { return (d >> sh) & 0x00FF00FFu; };
     st_stream(pres + blk * 32 + lane,
-              make_uint4(__byte_perm(d0.x, d0.y, 0x6420), __byte_perm(d0.z, d0.w, 0x6420),
-                         __byte_perm(d1.x, d1.y, 0x6420), __byte_perm(d1.z, d1.w, 0x6420)));
+              make_uint4(__byte_perm(r(d0.x), r(d0.y), 0x6420), __byte_perm(r(d0.z), r(d0.w), 0x6420),
+                         __byte_perm(r(d1.x), r(d1.y), 0x6420), __byte_perm(r(d1.z), r(d1.w), 0x6420)));
+  }
   if (lane == 0) pbase[blk] = narrow ? base : kRawBlock;
 }
 
-// count_image over whole blocks (block b = the grid's warp b mod W, the
-// next block's two loads in flight while this one is coded and counted),
-// coding each block into the plane; the < 64 vectors past the last whole
-// block go to the last CTA, uncoded.
 // The coded count pass's last blocks, 8-block chunks taken warp by warp
 // from a counter (the next chunk's index requested while this one is
 // counted).  Out of line so its registers do not crowd the main loop.
 template <class Ctr>
 __device__ __noinline__ void count_tail_coded(const uint4* body, std::uint64_t static_end,
                                               std::uint32_t tail_chunks, std::uint32_t* ctail,
-                                              Ctr ctr, uint32_t* pbase, uint4* pres) {
+                                              Ctr ctr, uint32_t* pbase, uint4* pres, uint32_t sh) {
   constexpr std::uint64_t kWChunk = 8;
   const uint32_t lane = threadIdx.x & 31u;
   std::uint32_t c = 0;
@@ -679,13 +724,13 @@ __device__ __noinline__ void count_tail_coded(const uint4* body, std::uint64_t s
     for (std::uint64_t j = 0; j < kWChunk; j += 2) {
       qb0 = ld_stream(body + ((b0 + j + 1) << 6) + lane);
       qb1 = ld_stream(body + ((b0 + j + 1) << 6) + 32 + lane);
-      code_block(qa0, qa1, b0 + j, lane, pbase, pres);
+      code_block(qa0, qa1, b0 + j, lane, pbase, pres, sh);
       ctr.pair(qa0, qa1);
       if (j + 2 < kWChunk) {
         qa0 = ld_stream(body + ((b0 + j + 2) << 6) + lane);
         qa1 = ld_stream(body + ((b0 + j + 2) << 6) + 32 + lane);
       }
-      code_block(qb0, qb1, b0 + j + 1, lane, pbase, pres);
+      code_block(qb0, qb1, b0 + j + 1, lane, pbase, pres, sh);
       ctr.pair(qb0, qb1);
     }
     c = __shfl_sync(0xFFFFFFFFu, nc, 0);
@@ -696,7 +741,7 @@ template <class Ctr>
 __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std::uint64_t n,
                                                   int cta, int ctas, const Ctr& ctr,
                                                   uint32_t* pbase, uint4* pres,
-                                                  std::uint32_t* ctail) {
+                                                  std::uint32_t* ctail, uint32_t sh) {
   const std::uint64_t head = head_len(img, n);
   const std::uint64_t nvec = (n - head) >> 3;
   const std::uint64_t nblk = nvec >> 6;
@@ -719,7 +764,7 @@ __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std:
     x1 = ld_stream(body + (blk << 6) + 32 + lane);
   };
   auto work = [&](std::uint64_t blk, uint4 x0, uint4 x1) {
-    code_block(x0, x1, blk, lane, pbase, pres);
+    code_block(x0, x1, blk, lane, pbase, pres, sh);
     ctr.pair(x0, x1);
   };
   // the last ~3% of the blocks are handed out dynamically (count_tail_coded):
@@ -736,7 +781,7 @@ __device__ __forceinline__ void count_image_coded(const std::uint16_t* img, std:
     work(b, qb0, qb1);
     b += W;
   }
-  if (tail_chunks != 0) count_tail_coded(body, static_end, tail_chunks, ctail, ctr, pbase, pres);
+  if (tail_chunks != 0) count_tail_coded(body, static_end, tail_chunks, ctail, ctr, pbase, pres, sh);
 }
 
 // Block vectors as loaded for the apply: a narrow block's residuals (r0,
@@ -756,19 +801,20 @@ __device__ __forceinline__ void load_block(const uint4* body, const uint4* pres,
         "=r"(r1.w)
       : "r"(bw), "r"(kRawBlock), "l"(pr), "l"(p0), "l"(p1));
 }
-__device__ __forceinline__ uint4 expand(uint32_t lo, uint32_t hi, uint32_t b2) {
-  // base + residual <= 65535 per half: no carry between the halves
-  return make_uint4(__byte_perm(lo, 0u, 0x4140) + b2, __byte_perm(lo, 0u, 0x4342) + b2,
-                    __byte_perm(hi, 0u, 0x4140) + b2, __byte_perm(hi, 0u, 0x4342) + b2);
+__device__ __forceinline__ uint4 expand(uint32_t lo, uint32_t hi, uint32_t b2, uint32_t sh) {
+  // base + (residual << sh) <= 65535 per half (sh <= 8): no carry between halves
+  return make_uint4((__byte_perm(lo, 0u, 0x4140) << sh) + b2, (__byte_perm(lo, 0u, 0x4342) << sh) + b2,
+                    (__byte_perm(hi, 0u, 0x4140) << sh) + b2, (__byte_perm(hi, 0u, 0x4342) << sh) + b2);
 }
 template <int kSwz>
 __device__ __forceinline__ void store_block(const std::uint16_t* s_lut, uint4* dst, std::uint64_t b,
-                                            uint32_t lane, uint32_t bw, uint4 r0, uint4 r1) {
+                                            uint32_t lane, uint32_t bw, uint4 r0, uint4 r1,
+                                            uint32_t sh) {
   uint4 v0 = r0, v1 = r1;
   if (bw != kRawBlock) {
     const uint32_t b2 = bw * 0x10001u;
-    v0 = expand(r0.x, r0.y, b2);
-    v1 = expand(r0.z, r0.w, b2);
+    v0 = expand(r0.x, r0.y, b2, sh);
+    v1 = expand(r0.z, r0.w, b2, sh);
   }
   st_stream(dst + (b << 6) + lane, lookup_vec<kSwz>(s_lut, v0));
   st_stream(dst + (b << 6) + 32 + lane, lookup_vec<kSwz>(s_lut, v1));
@@ -784,7 +830,7 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
                                                   const std::uint16_t* in, std::uint16_t* out,
                                                   std::uint64_t n, int cta, int ctas,
                                                   std::uint32_t* tail, const uint32_t* pbase,
-                                                  const uint4* pres) {
+                                                  const uint4* pres, uint32_t sh) {
   constexpr std::uint64_t kWarps = kThreads / 32;
   constexpr std::uint64_t kChunkBlk = 4 * kWarps;  // blocks per tail chunk (128 KiB of image)
   const std::uint64_t tid = static_cast<std::uint64_t>(cta) * kThreads + threadIdx.x;
@@ -835,7 +881,7 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
       for (int u = 0; u < kU; ++u) nnbw[u] = __ldcg(pbase + MAPB(nx + (kU + u) * W));
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) store_block<kSwz>(s_lut, dst, MAPB(b + u * W), lane, bw[u], r[u][0], r[u][1]);
+    for (int u = 0; u < kU; ++u) store_block<kSwz>(s_lut, dst, MAPB(b + u * W), lane, bw[u], r[u][0], r[u][1], sh);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       r[u][0] = nr[u][0];
@@ -850,7 +896,7 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
     const uint32_t w = __ldcg(pbase + MAPB(b));
     uint4 y0, y1;
     load_block(src, pres, MAPB(b), lane, w, y0, y1);
-    store_block<kSwz>(s_lut, dst, MAPB(b), lane, w, y0, y1);
+    store_block<kSwz>(s_lut, dst, MAPB(b), lane, w, y0, y1, sh);
   }
   if (!dynamic) return;
   __shared__ std::uint32_t s_chunk;
@@ -868,7 +914,7 @@ __device__ __forceinline__ void apply_image_coded(const std::uint16_t* s_lut,
 #pragma unroll
     for (int u = 0; u < 4; ++u) load_block(src, pres, MAPB(b0 + u * kWarps), lane, w[u], y[u][0], y[u][1]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) store_block<kSwz>(s_lut, dst, MAPB(b0 + u * kWarps), lane, w[u], y[u][0], y[u][1]);
+    for (int u = 0; u < 4; ++u) store_block<kSwz>(s_lut, dst, MAPB(b0 + u * kWarps), lane, w[u], y[u][0], y[u][1], sh);
   }
 }
 #undef MAPB
@@ -1048,8 +1094,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   LUT_STAMP(0);
   const bool count = stages & kCount;
   // smem layout of this launch (the same in every CTA: a fixed sample of img)
-  __shared__ uint32_t s_swz, s_wlo;
-  if ((stages & (kCount | kApply)) != 0) sample_layout(img, n, &s_swz, &s_wlo);
+  __shared__ uint32_t s_swz, s_wlo, s_wsh;
+  if ((stages & (kCount | kApply)) != 0) sample_layout(img, n, &s_swz, &s_wlo, &s_wsh);
   if (!count) __syncthreads();  // else published by the zeroing's barrier
   // ---- phase 1: per-CTA histograms
   uint32_t* win = bins + kWords;  // the u32 window after the packed bins
@@ -1058,16 +1104,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       smem_u4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     const bool coded = plane != nullptr && (s_swz & 8u) != 0;
+    const uint32_t psh = (s_swz >> 8) & 15u;  // the plane's residual shift
     auto run = [&](const auto& ctr) {
-      if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres, tail + 1);
+      if (coded) count_image_coded(img, n, blockIdx.x, nparts, ctr, pbase, pres, tail + 1, psh);
       else count_image(img, n, blockIdx.x, nparts, ctr);
     };
     // the window serves repetitive data too (flat / few-level images within
     // its span): red.shared of many lanes on one u32 counter runs at the
     // HBM rate (tools/hist_probe.cu mode 2), with no warp-combining probe
-    const bool windowed = (s_swz & 3u) == 0 && s_wlo != kNoWindow;
-    switch (windowed ? 0xFFu : (s_swz & 7u)) {
-      case 0xFF: run(WindowCounter{bins, overflow, win, s_wlo}); break;
+    const bool windowed = s_wlo != kNoWindow;
+    const uint32_t lay = s_swz & 3u;
+    switch (windowed ? 8u + lay : (s_swz & 7u)) {
+      case 8: run(WindowCounter<0>{bins, overflow, win, s_wlo, s_wsh}); break;
+      case 9: run(WindowCounter<1>{bins, overflow, win, s_wlo, s_wsh}); break;
+      case 10: run(WindowCounter<2>{bins, overflow, win, s_wlo, s_wsh}); break;
       case 0: run(PlainCounter<0>{bins, overflow}); break;
       case 1: run(PlainCounter<1>{bins, overflow}); break;
       case 2: run(PlainCounter<2>{bins, overflow}); break;
@@ -1077,7 +1127,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (windowed) {
       __syncthreads();
-      fold_window(bins, overflow, win, s_wlo);
+      if (lay == 1) fold_window<1>(bins, overflow, win, s_wlo, s_wsh);
+      else if (lay == 2) fold_window<2>(bins, overflow, win, s_wlo, s_wsh);
+      else fold_window<0>(bins, overflow, win, s_wlo, s_wsh);
     }
     __syncthreads();
     LUT_STAMP(1);
@@ -1282,10 +1334,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   else stage_lut<0>(smem_u4, lut);
   __syncthreads();
   LUT_STAMP(8);
+  const uint32_t psh = (s_swz >> 8) & 15u;
   if (plane != nullptr && (s_swz & 8u) != 0) {  // the plane this launch's count pass coded
-    if (layout == 1) apply_image_coded<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
-    else if (layout == 2) apply_image_coded<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
-    else apply_image_coded<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres);
+    if (layout == 1) apply_image_coded<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres, psh);
+    else if (layout == 2) apply_image_coded<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres, psh);
+    else apply_image_coded<0>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail, pbase, pres, psh);
   } else {
     if (layout == 1) apply_image<1>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);
     else if (layout == 2) apply_image<2>(s_lut, img, out, n, blockIdx.x, gridDim.x, tail);

@@ -146,3 +146,28 @@ def test_plane_flat_and_binary_scenes(gpu):
         D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
         assert np.array_equal(u16(out), ref_out)
         assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
+
+
+@pytest.mark.parametrize("shift", [2, 4, 8])
+@pytest.mark.parametrize("outliers", [False, True])
+def test_plane_and_window_shifted_for_msb_aligned_smooth_data(gpu, shift, outliers):
+    """Smooth MSB-aligned data (a ramp in steps of 2^shift): the layout
+    sample picks the shifted u32 window (counter v >> shift) and the shifted
+    plane (residual (v - base) >> shift); off-grid samples fall back to the
+    packed bins / raw blocks."""
+    torch, D = _dev()
+    n = PLANE_MIN + 4099
+    rng = np.random.default_rng(shift)
+    span = 3000 if shift < 8 else 200
+    base = (np.arange(n, dtype=np.int64) * span) // n + rng.integers(0, 40, n)
+    vals = (np.minimum(base, (65535 >> shift)) << shift).astype(np.uint16)
+    if outliers:
+        idx = rng.integers(0, n, n // 5000)
+        vals[idx] = vals[idx] | 1   # off the 2^shift grid
+    img = torch.from_numpy(vals.view(np.int16)).to(gpu)
+    ref_out, ref_lut, ref_st = O.lut_correct(vals, O.LUT_EQUALIZE)
+    out = torch.empty_like(img)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+    assert np.array_equal(u16(out), ref_out)
+    assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st

@@ -18,6 +18,7 @@ imgs = {
     "msb12_x16": lambda: (torch.randint(0, 4096, (n,), device="cuda", generator=g, dtype=torch.int16) * 16),
     "msb10_x64": lambda: (torch.randint(0, 1024, (n,), device="cuda", generator=g, dtype=torch.int16) * 64),
     "msb8_x256": lambda: (torch.randint(0, 256, (n,), device="cuda", generator=g, dtype=torch.int32) * 256).to(torch.int16),
+    "ramp12_x16": lambda: ((D.synth_image(0, 0x5EED, 32768, 32768).to(torch.int32) - 900) * 16).to(torch.int16),
     "half_flat": lambda: torch.where(torch.arange(n, device="cuda") < n // 2, torch.tensor(500, dtype=torch.int16, device="cuda"),
                                      D.synth_image(0, 0x5EED, 32768, 32768)),
 }
