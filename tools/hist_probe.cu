@@ -25,6 +25,8 @@
 //      no packing, no wraps) with red.shared; the rest to red.global
 //   18 mode 17 with returning atom (old value folded into a dummy)
 //   19 mode 0 through atomicAdd (compiler-emitted RED, no asm memory clobber)
+//   20 u32 red over 32768 counters indexed v & 32767 (timing only: what one
+//      SM of a pair holding half the bins as u32 would see on random data)
 #include <cstdint>
 #include <cstdio>
 #include <vector>
@@ -108,6 +110,8 @@ __global__ void __launch_bounds__(1024, 1) hist(const uint16_t* img, uint64_t n,
       if (d < 16384u) dummy ^= atomicAdd(bins + d, 1u); else redg(mine + v, 1);
     } else if (MODE == 19) {
       atomicAdd(bins + (v >> 1), inc);
+    } else if (MODE == 20) {
+      atomicAdd(bins + (v & 32767u), 1u);
     }
     else if (MODE == 12) { if ((slot & 15) == 15) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
     else if (MODE == 13) { if ((slot & 31) == 31) redg(mine + v, 1); else reds(bins, v >> 1, inc); }
@@ -205,6 +209,7 @@ int main() {
     run<17>("17 u32 window red", img, n, parts, gh, sms);
     run<18>("18 u32 window atom (return)", img, n, parts, gh, sms);
     run<19>("19 packed u16 via atomicAdd", img, n, parts, gh, sms);
+    run<20>("20 u32 red, 32768 counters", img, n, parts, gh, sms);
   }
   return 0;
 }
