@@ -171,3 +171,18 @@ def test_plane_and_window_shifted_for_msb_aligned_smooth_data(gpu, shift, outlie
     D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
     assert np.array_equal(u16(out), ref_out)
     assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
+
+
+@pytest.mark.parametrize("delta", [-1, 0, 1])
+def test_plane_threshold(gpu, delta):
+    """Just below / at / above 2^25 samples (the plane starts at 2^25): the
+    same bytes as the oracle either way."""
+    torch, D = _dev()
+    n = PLANE_MIN + delta
+    img = D.synth_image(O.IMG_RAMP12, 11, 1, n)
+    ref_out, ref_lut, ref_st = O.lut_correct(u16(img), O.LUT_EQUALIZE)
+    out = torch.empty_like(img)
+    lut, stats, ws = D.new_lut(), D.new_stats(), D.lut_workspace(n)
+    D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
+    assert np.array_equal(u16(out), ref_out)
+    assert np.array_equal(u16(lut), ref_lut) and D.read_stats(stats) == ref_st
