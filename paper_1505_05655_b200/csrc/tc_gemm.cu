@@ -95,6 +95,30 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
   }
 }
 
+// The epilogue's wait for an accumulator (~a tile's mainloop, 100s of us):
+// back off with __nanosleep between probes so the four waiting warps do not
+// spin (power-capped GEMM: idle issue slots are energy the clock can use).
+__device__ __forceinline__ void mbar_wait_sleepy(std::uint64_t* bar, std::uint32_t parity) {
+  const std::uint32_t addr = smem_u32(bar);
+  std::uint32_t done = 0;
+  std::uint64_t t0 = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+#ifndef GPCX_NO_SLEEPY
+    __nanosleep(2000);
+#endif
+    if (t0 == 0) t0 = global_ns();
+    else if (global_ns() - t0 > 10000000000ull) __trap();
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, std::uint64_t* bar, void* dst,
                                             int x, int y) {
   asm volatile(
@@ -300,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int mb, nb;
       tm.coords(t, mb, nb);
-      mbar_wait(&tmem_full[acc], acc_phase);
+      mbar_wait_sleepy(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * BM + quarter * 32 + lane;
       float* crow = C + static_cast<std::uint64_t>(row) * ldc;
@@ -536,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int t = pair; t < ntiles; t += npairs) {
       int mb, nb;
       tm.coords(t, mb, nb);
-      mbar_wait(&tmem_full[acc], acc_phase);
+      mbar_wait_sleepy(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
       float* crow = C + static_cast<std::uint64_t>(row) * ldc;
