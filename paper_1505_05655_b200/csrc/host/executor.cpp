@@ -159,7 +159,11 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
       // the band histogram stays in HBM; phase 2 sums the bands' histograms
       // with P2P loads (lut::launch_correct_from_peers) after every band's
       // `ready` event -- no device -> host -> device round trip
-      lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream);
+      // with the apply to follow, the count also codes the band's residual
+      // plane for it (a plane-sized workspace; launch_correct_from_peers)
+      if (need_apply) s.lut_ws.ensure(lut::workspace_bytes(bn), /*zero=*/true);
+      lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream,
+                       need_apply ? s.lut_ws.cap : 0);
       GPCX_CUDA(cudaEventRecord(s.ready, s.stream));
     } else if (equalize) {
       lut::launch_hist(s.a.as<std::uint16_t>(), bn, s.d_hist(), s.lut_ws.ptr, s.stream);
@@ -221,7 +225,7 @@ gpcx_lut_stats lut_host(Flag flag, const task::LutParams& p, const std::uint16_t
                                   cudaMemcpyHostToDevice, s.stream));
         lut::launch_correct_from_peers(s.d_peer_table(), 0, p.mode, dimg,
                                        need_apply ? dimg : nullptr, bn, s.d_lut(), s.d_stats(),
-                                       s.lut_ws.ptr, s.stream);
+                                       s.lut_ws.ptr, s.stream, need_apply ? s.lut_ws.cap : 0);
       } else if (equalize) {
         GPCX_CUDA(cudaMemcpyAsync(s.d_hist(), global_hist.data(), 65536 * 4,
                                   cudaMemcpyHostToDevice, s.stream));

@@ -73,14 +73,18 @@ void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::u
                          void* ws, cudaStream_t stream, std::uint64_t ws_bytes = 0);
 // Host-ordered second half for the in-process planner: sum the group's
 // published histograms (table->flags unused), LUT, apply the band.
+// ws_bytes (optional): the band's count launch (launch_hist with the same
+// ws_bytes, same image and workspace) coded the residual plane, read here.
 void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mode,
                                const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
                                std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
-                               cudaStream_t stream);
+                               cudaStream_t stream, std::uint64_t ws_bytes = 0);
 
-// Histogram of img into hist (u32[65536]).
+// Histogram of img into hist (u32[65536]).  ws_bytes >= workspace_bytes(n)
+// also codes the residual plane for a later launch_correct_from_peers of the
+// same image and workspace (the in-process planner); 0 never does.
 void launch_hist(const std::uint16_t* img, std::uint64_t n, std::uint32_t* hist,
-                 void* ws, cudaStream_t stream);
+                 void* ws, cudaStream_t stream, std::uint64_t ws_bytes = 0);
 // LUT + stats from a merged histogram (`ws` is a LUT workspace, used for the
 // per-slice scan summaries).
 void launch_from_hist(const std::uint32_t* hist, int mode, std::uint16_t* lut,

@@ -1638,9 +1638,12 @@ void launch_fused(int stages, const std::uint16_t* img, std::uint16_t* out, std:
                   unsigned long long timeout_ns = 0, std::uint64_t ws_bytes = 0) {
   set_attrs_once();
   auto* base = static_cast<unsigned char*>(ws);
-  // the residual plane: count and apply in this launch, a plane-sized workspace
+  // the residual plane, given a plane-sized workspace: count and apply in
+  // this launch, or a split pair (launch_hist -> launch_correct_from_peers
+  // on one workspace and image, the in-process planner) -- an apply-only
+  // launch handed ws_bytes reads the plane its count launch wrote
   unsigned char* plane = nullptr;
-  if ((stages & (kCount | kApply)) == (kCount | kApply) && plane_bytes(n) != 0 &&
+  if ((stages & (kCount | kApply)) != 0 && plane_bytes(n) != 0 &&
       ws_bytes >= workspace_bytes(n) && plane_enabled())
     plane = base + workspace_bytes();
   auto* overflow = reinterpret_cast<uint32_t*>(base + kOverflowOff);
@@ -1673,8 +1676,9 @@ bool co_aligned(const void* a, const void* b) {
 }  // namespace
 
 void launch_hist(const std::uint16_t* img, std::uint64_t n, uint32_t* hist,
-                 void* ws, cudaStream_t stream) {
-  launch_fused(kCount, img, nullptr, n, hist, GPCX_LUT_EQUALIZE, nullptr, nullptr, ws, stream);
+                 void* ws, cudaStream_t stream, std::uint64_t ws_bytes) {
+  launch_fused(kCount, img, nullptr, n, hist, GPCX_LUT_EQUALIZE, nullptr, nullptr, ws, stream,
+               nullptr, 0, 0, ws_bytes);
 }
 
 void launch_from_hist(const uint32_t* hist, int mode, std::uint16_t* lut,
@@ -1736,14 +1740,14 @@ void launch_correct_peer(const PeerTable* table, std::uint32_t* own_hist, std::u
   const bool fused_apply = out != nullptr && co_aligned(in, out);
   const int stages = kCount | kExchange | kBuild | (fused_apply ? kApply : 0);
   launch_fused(stages, in, fused_apply ? out : nullptr, n, own_hist, mode, lut, stats, ws,
-               stream, table, seq, timeout_ns, ws_bytes);
+               stream, table, seq, timeout_ns, fused_apply ? ws_bytes : 0);
   if (out != nullptr && !fused_apply) launch_apply(lut, in, out, n, stream);
 }
 
 void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mode,
                                const std::uint16_t* in, std::uint16_t* out, std::uint64_t n,
                                std::uint16_t* lut, gpcx_lut_stats* stats, void* ws,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, std::uint64_t ws_bytes) {
   if (out == nullptr || n == 0) {
     launch_fused(kExchange | kBuild, nullptr, nullptr, 0, nullptr, mode, lut, stats, ws, stream,
                  table, seq, 0);
@@ -1751,7 +1755,7 @@ void launch_correct_from_peers(const PeerTable* table, std::uint32_t seq, int mo
   }
   if (co_aligned(in, out)) {
     launch_fused(kExchange | kBuild | kApply, in, out, n, nullptr, mode, lut, stats, ws, stream,
-                 table, seq, 0);
+                 table, seq, 0, ws_bytes);
     return;
   }
   launch_fused(kExchange | kBuild, nullptr, nullptr, 0, nullptr, mode, lut, stats, ws, stream,

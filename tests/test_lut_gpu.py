@@ -434,3 +434,23 @@ def test_counter_wraps_every_count_variant(gpu, variant):
     D.lut_correct(img, out, O.LUT_EQUALIZE, lut, stats, ws)
     assert np.array_equal(u16(out), ref_out) and np.array_equal(u16(lut), ref_lut)
     assert D.read_stats(stats) == ref_st
+
+
+@pytest.mark.parametrize("kind", [O.IMG_RAMP12, O.IMG_UNIFORM16])
+def test_planner_bands_past_the_plane_threshold(gpu, kind):
+    """In-process planner with bands >= 2^25 samples: each band's count
+    launch codes its residual plane and the band's apply launch (after the
+    peer histogram sum) reads it -- same bytes as one device."""
+    rows, cols = 8192, 8200  # 2 bands of 4096 x 8200 = 33.6 M samples
+    img = O.synth_image(kind, 5, rows, cols)
+    r_out, r_lut, r_st = O.lut_correct(img, O.LUT_EQUALIZE)
+    try:
+        for g in (1, 2):
+            G.init([0] * g)
+            res, payload = G.run("LUT_CORRECT", f"rows={rows},cols={cols},mode=equalize", img)
+            assert np.array_equal(payload.view(np.uint16), r_out), g
+            assert int(res["lo"]) == r_st["lo"] and int(res["hi"]) == r_st["hi"]
+            res, payload = G.run("LUT_GEN", f"rows={rows},cols={cols},mode=equalize", img)
+            assert np.array_equal(payload.view(np.uint16), r_lut), g
+    finally:
+        G.init([0])
