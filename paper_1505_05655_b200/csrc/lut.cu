@@ -643,22 +643,21 @@ __device__ __forceinline__ void apply_image(const std::uint16_t* s_lut, const st
 // The packed-bin count pass is bound by the shared-memory atomic unit
 // (~0.47 ms at C3 against a 0.335 ms read floor: HBM idles ~30% of it), the
 // apply pass by HBM (2 B read + 2 B written per sample).  With room in the
-// workspace
-// (workspace_bytes(n)), the count pass also stores every 512-sample block
-// (64 vectors: two adjacent 512-byte warp loads) whose samples lie in a
-// 256-value window as a base word and one residual byte per sample
-// (code_block); the apply pass reads that 1 B/px copy instead of the
-// 2 B/px image.  Bytes move from the HBM-bound pass into the atomic-bound
-// one: 2 + 1 (count) and 1 + 2 (apply) per sample instead of 2 and 2 + 2 --
-// the same 6 B/px, but no pass idles HBM.  Other blocks (noise-like data)
-// get base word kRawBlock and are applied from the image.
+// workspace (workspace_bytes(n)), the count pass also stores every
+// 512-sample block (64 vectors: two adjacent 512-byte warp loads) whose
+// samples lie in a 256-value window as a base word and one residual byte
+// per sample (code_block); the apply pass reads that 1 B/px copy instead of
+// the 2 B/px image.  Bytes move from the HBM-bound pass into the
+// atomic-bound one: 2 + 1 (count) and 1 + 2 (apply) per sample instead of 2
+// and 2 + 2 -- the same 6 B/px, but no pass idles HBM.  Other blocks
+// (noise-like data) get base word kRawBlock and are applied from the image.
 // MSB-aligned smooth data (sample_layout's shift sh = min(tz, 8)) is coded
 // in steps of 2^sh: window [base, base + 256 << sh), residual
 // (v - base) >> sh.  Exact by construction: v = base + (residual << sh).
-// Block b = vectors
-// [64b, 64b + 64) of the 16-byte-aligned body, lane l holding vectors
-// 64b + l and 64b + 32 + l (residuals: 16 bytes at plane vector 32b + l);
-// plane layout: u32 base[n >> 9] (256-byte rounded) | 512 bytes per block.
+// Block b = vectors [64b, 64b + 64) of the 16-byte-aligned body, lane l
+// holding vectors 64b + l and 64b + 32 + l (residuals: 16 bytes at plane
+// vector 32b + l); plane layout: u32 base[n >> 9] (256-byte rounded) | 512
+// bytes per block.
 constexpr uint32_t kRawBlock = 0x10000u;
 constexpr std::uint64_t kPlaneMin = 1ull << 25;  // samples; below it the image stays in L2
 
@@ -681,9 +680,9 @@ __device__ __forceinline__ uint4 ld_plane(const uint4* p) {
 // q - base (per u16 half): a half outside the window or off the grid
 // leaves a bit outside [sh, sh + 8) set in its half (an underflowing low
 // half included, given the clamp), and with none outside there is no
-// borrow, so bits [sh, sh + 8) of each half are the residuals.  One shuffle and one vote per block, no min/max
-// tree (the count pass is issue-sensitive: +35 instructions per block of a
-// redux min/max version cost ~75 us at C3).
+// borrow, so bits [sh, sh + 8) of each half are the residuals.  One
+// shuffle and one vote per block, no min/max tree (a redux min/max version
+// cost the then issue-sensitive count pass ~75 us at C3).
 __device__ __forceinline__ void code_block(uint4 q0, uint4 q1, std::uint64_t blk, uint32_t lane,
                                            uint32_t* pbase, uint4* pres, uint32_t sh) {
   // sh > 0 (MSB-aligned data, steps of 2^sh): window [base, base + 256 << sh),
