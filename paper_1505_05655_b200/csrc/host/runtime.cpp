@@ -167,7 +167,7 @@ void Runtime::init(const std::vector<int>& devices) {
     int count = 0;
     GPCX_CUDA(cudaGetDeviceCount(&count));
     if (d < 0 || d >= count) fail(Errc::BadValue, "device " + std::to_string(d) + " not present");
-    pools_.push_back(Pool{d, {}, {}});
+    pools_.push_back(Pool{d, {}, {}, true, {}});
   }
   enable_peer_access(want);
   inited_ = true;
@@ -186,7 +186,7 @@ void Runtime::ensure_init_locked() {
   if (count <= 0) fail(Errc::TaskFailed, "no CUDA device available");
   std::vector<int> all;
   for (int i = 0; i < count; ++i) {
-    pools_.push_back(Pool{i, {}, {}});
+    pools_.push_back(Pool{i, {}, {}, true, {}});
     all.push_back(i);
   }
   enable_peer_access(all);

@@ -665,14 +665,6 @@ __host__ __device__ __forceinline__ std::uint64_t plane_base_bytes(std::uint64_t
   return ((n >> 9) * 4 + 255) & ~std::uint64_t{255};
 }
 
-__device__ __forceinline__ uint4 ld_plane(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
 // One block (the warp's 64 vectors, all lanes active).  Base = lane 0's
 // first sample - (128 << sh) (clamped to [0, 65536 - (256 << sh)]); the
 // block is narrow when every sample lies on the 2^sh grid in
